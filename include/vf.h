@@ -1,0 +1,196 @@
+/* include/vf.h — C ABI of the B200 hybrid-voxel-format first-hit tracer (libvf.so).
+ *
+ * The calls follow the paper's statement of the problem (arXiv 2410.14128, PAPER.md):
+ *   - construction maps a voxel source + a hybrid format to one word-addressable buffer
+ *     (§4.1 "Hybrid Format Construction"; layout PAPER.md:84-162, §3.3);
+ *   - intersection maps (buffer, ray) to "whether the ray hits a single voxel", visiting
+ *     sub-volumes "in order of hit time" (§4.2), here narrowed/extended
+ *     to the hit voxel coordinate, its entry t and a miss flag.
+ *
+ * Conventions
+ *   - No exception crosses this boundary. Every call returns vf_status; details of the
+ *     last failure on the calling thread via vf_last_error().
+ *   - Coordinates are grid units: voxel (i,j,k) occupies [i,i+1)x[j,j+1)x[k,k+1); the
+ *     volume is [0,Rx)x[0,Ry)x[0,Rz). There is no world transform (reading A1).
+ *   - Hit semantics are the exact "right-limit" definition of SURVEY.md §8(c) c-1: the
+ *     first non-empty voxel (empty iff all 32 bits are 0) pierced by
+ *     p(t) = o + t d over [tmin, tmax); plane crossings with equal exact t step together.
+ *     Exactness (bit-exact x,y,z and miss flag; t within 1e-4 relative) is guaranteed for
+ *     rays in the canonical domain: R <= 4096 per axis; |o_a| in {0} U [2^-16, 2^20);
+ *     |d_a| in {0} U [2^-30, 2], d != 0; 0 <= tmin < tmax; tmin and finite tmax in
+ *     {0} U [2^-16, 2^20); tmax = +inf allowed. Rays outside it are traced, not rejected.
+ *   - All device pointers must be on the handle's device and 16-byte aligned.
+ */
+#ifndef VF_H
+#define VF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VF_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define VF_API __attribute__((visibility("default")))
+#else
+#define VF_API
+#endif
+
+typedef enum {
+  VF_OK = 0,
+  VF_ERR_INVALID_ARG = 1, /* null/misaligned pointer, bad size, bad volume */
+  VF_ERR_PARSE = 2,       /* signature syntax; message gives the character position */
+  VF_ERR_FORMAT = 3,      /* non-cubic or non-power-of-two non-first level,
+                             depth 0, resolution != volume dims, more than VF_MAX_TIERS tiers */
+  VF_ERR_UNSUPPORTED = 4, /* valid paper format this build does not implement (DF, D(...)) */
+  VF_ERR_OVERFLOW = 5,    /* a stored offset would reach 2^32 words (PAPER.md:86, 16 GiB) */
+  VF_ERR_OOM = 6,         /* device allocation failed */
+  VF_ERR_CUDA = 7         /* CUDA runtime / launch error */
+} vf_status;
+
+/* Thread-local message for the last failing call on this thread ("" if none). Valid until
+ * the next vf_* call on the same thread. */
+VF_API const char* vf_last_error(void);
+VF_API int vf_abi_version(void);
+
+/* ---------------------------------------------------------------- format description
+ * A hybrid format is an ordered list of levels, level 1 (highest) first (PAPER.md:63-82,
+ * §3.2, Table 1). Each level is one base format:
+ *   VF_RAW   R(W,H,D): 2^W x 2^H x 2^D grid of terminating integers
+ *   VF_SVO   S(L)    : sparse voxel octree of depth L, 2-word nodes
+ *   VF_SVDAG G(L)    : de-duplicated octree of depth L, 1..9-word nodes
+ *   VF_NTREE T(n,d)  : N^3-tree, N = 2^n, depth d, 16-B nodes with a 64-bit occupancy mask
+ *                      (generalisation of SVO; layout is ours)
+ *   VF_DF    D(W,H,D,M): distance field — parsed, not implemented
+ *                      (VF_ERR_UNSUPPORTED), SURVEY §8(f) NEXT item 1.
+ * Every level but the first must be cubic with power-of-two extent. */
+enum { VF_RAW = 0, VF_SVO = 1, VF_SVDAG = 2, VF_NTREE = 3, VF_DF = 4 };
+
+typedef struct {
+  uint32_t kind;           /* VF_RAW, VF_SVO, VF_SVDAG, VF_NTREE, VF_DF */
+  uint8_t log2_extent[3];  /* Raw / DF: W, H, D */
+  uint8_t depth;           /* SVO / SVDAG: L; NTree: d */
+  uint8_t log2_fanout;     /* NTree: n (N = 2^n, n in {1,2}) */
+  uint8_t df_max;          /* DF: M */
+  uint8_t reserved[2];
+} vf_level;
+
+#define VF_MAX_LEVELS 16
+#define VF_MAX_TIERS 16 /* a tier = one node level: Raw 1, S(L)/G(L) L, T(n,d) d */
+
+/* Parse a signature: "R(3,3,3) G(8)", Table-2 sugar "R(3^3) G(8)" / "R(3³) G(8)" (PAPER.md
+ * Table 2, :303-322), "S(11)", "T(2,2) T(2,1) R(4^3)", "D(4^3, 6) G(5)" (parsed, then
+ * unsupported at build). Whitespace-separated levels; whitespace inside parentheses allowed.
+ * out: caller array of capacity cap; *n_out = number of levels. VF_ERR_PARSE on syntax. */
+VF_API vf_status vf_parse_format(const char* sig, vf_level* out, uint32_t cap, uint32_t* n_out);
+
+/* Canonical signature text ("R(3, 3, 3) G(8)"); parse(to_string(f)) == f. */
+VF_API vf_status vf_format_to_string(const vf_level* levels, uint32_t n_levels, char* buf, size_t cap);
+
+/* Validate a level list and return its total resolution per axis (product of per-level
+ * extents, "R(1, 0, 2) R(2, 2, 2)" -> 8 x 4 x 16). */
+VF_API vf_status vf_format_resolution(const vf_level* levels, uint32_t n_levels, uint32_t dims[3]);
+
+/* ---------------------------------------------------------------- volume input */
+enum {
+  VF_VOL_DENSE_DEVICE = 0, /* rgba: device, x-fastest (x + Rx*(y + Ry*z)), 0 = empty */
+  VF_VOL_SPARSE_DEVICE = 1 /* n_voxels entries: keys (x | y<<21 | z<<42) and non-zero rgba
+                              values, device arrays, any order, no duplicate keys */
+};
+
+typedef struct {
+  uint32_t kind;
+  uint32_t dims[3];
+  const uint32_t* rgba;   /* DENSE: borrowed for the duration of vf_build */
+  uint64_t n_voxels;      /* SPARSE */
+  const uint64_t* keys;   /* SPARSE: borrowed */
+  const uint32_t* values; /* SPARSE: borrowed */
+} vf_volume;
+
+/* ---------------------------------------------------------------- build */
+typedef struct vf_handle vf_handle; /* opaque; owns the format buffer; immutable after build */
+
+enum {
+  VF_BUILD_WHOLE_LEVEL_DEDUP = 1u << 0, /* one SVDAG de-dup map per level across sub-volumes
+                                           (§4.3; evaluated ON).
+                                           Clear it for per-sub-volume maps (ablation). */
+  VF_BUILD_DEFAULT = VF_BUILD_WHOLE_LEVEL_DEDUP
+};
+
+/* Build the format buffer on `device` (stream-ordered on cuda_stream, synchronous before
+ * return). Buffer layout is the paper's: u32 words, word 0 = root pointer
+ * (0 for an empty volume, buffer [0]); terminating integers are word offsets to the next
+ * level's sub-volume or RGBA at the finest level; empty children are 0. Two alignment
+ * paddings are added (reported in vf_stats.paper_layout_bytes vs bytes_used): SVO children
+ * blocks start at even words (8-B node loads), N^3-tree nodes at multiples of 4 words (16-B).
+ * *bytes_used = 4 x device words including word 0. Level 1's resolution must equal dims.
+ * On error *out is NULL and nothing is leaked. */
+VF_API vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_levels, uint32_t build_flags,
+                   int device, void* cuda_stream, vf_handle** out, uint64_t* bytes_used);
+
+/* ---------------------------------------------------------------- trace (the hot path) */
+typedef struct {
+  float ox, oy, oz, tmin, dx, dy, dz, tmax;
+} vf_ray; /* 32 B, grid units */
+
+typedef struct {
+  int32_t x, y, z;
+  float t;
+} vf_hit; /* 16 B; miss: x = y = z = -1, t = +inf */
+
+enum {
+  VF_TRACE_RESTART_SV = 1u << 0 /* "restarting sparse voxel intersection" (§4.3):
+                                   stackless — after leaving a node of an SVO / SVDAG / N^3-tree
+                                   level, re-descend from that level's sub-volume root instead
+                                   of popping a per-thread stack. Results are identical. */
+};
+
+/* Trace n rays (device array) into hits (device array), one thread per ray, asynchronously
+ * on cuda_stream; hits are valid after the stream synchronises. Concurrent traces on one
+ * handle are allowed (read-only). n = 0 is a no-op. */
+VF_API vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t trace_flags,
+                   void* cuda_stream);
+
+/* End-to-end variant with HOST buffers: copies rays host->device, traces, copies hits
+ * device->host, synchronises the stream before returning. Staging device memory is owned
+ * by the handle (grown on demand; calls on one handle must not overlap). Host buffers
+ * should be pinned (cudaHostAlloc / torch pin_memory) for full copy bandwidth. */
+VF_API vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hit* host_hits, uint32_t trace_flags,
+                        void* cuda_stream);
+
+/* ---------------------------------------------------------------- test aids */
+/* Point query (S:400-406 analogue): rgba_out[i] = stored voxel at xyz[3i..3i+2] (device
+ * uint32 triples), 0 if empty or out of range; descends the format like intersection. */
+VF_API vf_status vf_query(const vf_handle* h, const uint32_t* xyz, uint64_t n, uint32_t* rgba_out, void* cuda_stream);
+
+typedef struct {
+  uint64_t bytes_used;         /* device buffer bytes (4 x words incl. word 0) */
+  uint64_t paper_layout_bytes; /* same without alignment padding (the paper's layout) */
+  uint64_t nonempty_voxels;
+  uint32_t dims[3];
+  uint32_t n_levels;
+  uint32_t n_tiers;
+  uint32_t root;                 /* word 0 */
+  uint64_t nodes_per_tier[VF_MAX_TIERS]; /* stored nodes per tier (unique nodes for SVDAG) */
+  uint64_t words_per_tier[VF_MAX_TIERS]; /* paper-layout words written by each tier */
+  uint64_t dedup_leaf_nodes;   /* SVDAG 1-word leaf nodes stored (all SVDAG levels) */
+  double build_ms;             /* wall time of vf_build */
+} vf_stats;
+
+VF_API vf_status vf_stats_get(const vf_handle* h, vf_stats* out);
+
+/* Device pointer to the format buffer and its word count (read-only; for tests and tools). */
+VF_API vf_status vf_buffer(const vf_handle* h, const uint32_t** words, uint64_t* n_words);
+
+/* Copy words [first, first + count) of the format buffer to host memory (synchronous). */
+VF_API vf_status vf_buffer_read(const vf_handle* h, uint64_t first, uint64_t count, uint32_t* host_out);
+
+VF_API void vf_destroy(vf_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VF_H */

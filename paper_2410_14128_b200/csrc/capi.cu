@@ -1,0 +1,205 @@
+// capi.cu — the extern "C" boundary of libvf.so (include/vf.h). No exception crosses it.
+#include <stdint.h>
+#include <string.h>
+
+#include <new>
+
+#include "vf_internal.cuh"
+
+using namespace vf;
+
+struct vf_handle : vf::Handle {};
+
+namespace {
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_levels, uint32_t build_flags, int device,
+                   void* cuda_stream, vf_handle** out, uint64_t* bytes_used) {
+  clear_error();
+  if (out) *out = nullptr;
+  if (!vol || !levels || !out) {
+    set_error("vf_build: null argument");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (vol->kind != VF_VOL_DENSE_DEVICE && vol->kind != VF_VOL_SPARSE_DEVICE) {
+    set_error("vf_build: unknown volume kind %u", vol->kind);
+    return VF_ERR_INVALID_ARG;
+  }
+  if (vol->kind == VF_VOL_DENSE_DEVICE && !vol->rgba) {
+    set_error("vf_build: dense volume without rgba pointer");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (vol->kind == VF_VOL_SPARSE_DEVICE && vol->n_voxels && (!vol->keys || !vol->values)) {
+    set_error("vf_build: sparse volume without keys/values");
+    return VF_ERR_INVALID_ARG;
+  }
+  Format f;
+  vf_status st = expand_format(levels, n_levels, &f);
+  if (st != VF_OK) return st;
+  for (int a = 0; a < 3; ++a)
+    if (f.dims[a] != vol->dims[a]) {
+      set_error("vf_build: format resolution %ux%ux%u != volume dims %ux%ux%u", f.dims[0], f.dims[1], f.dims[2],
+                vol->dims[0], vol->dims[1], vol->dims[2]);
+      return VF_ERR_FORMAT;
+    }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    set_error("vf_build: CUDA device %d not available (%d devices)", device, ndev);
+    return VF_ERR_CUDA;
+  }
+  DeviceGuard g(device);
+  vf_handle* h = new (std::nothrow) vf_handle();
+  if (!h) {
+    set_error("vf_build: host allocation failed");
+    return VF_ERR_OOM;
+  }
+  h->device = device;
+  h->fmt = f;
+  memset(&h->stats, 0, sizeof(h->stats));
+  st = build_format(vol, f, build_flags, (cudaStream_t)cuda_stream, h);
+  if (st != VF_OK) {
+    if (h->buf) cudaFree(h->buf);
+    delete h;
+    return st;
+  }
+  h->tp = make_trace_params(f, h->stats.root);
+  for (int a = 0; a < 3; ++a) h->stats.dims[a] = f.dims[a];
+  h->stats.n_levels = f.n_levels;
+  h->stats.n_tiers = f.n_tiers;
+  if (bytes_used) *bytes_used = h->stats.bytes_used;
+  *out = h;
+  return VF_OK;
+}
+
+vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t trace_flags,
+                   void* cuda_stream) {
+  clear_error();
+  if (!h) {
+    set_error("vf_trace: null handle");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (n == 0) return VF_OK;
+  if (!rays || !hits || !aligned16(rays) || !aligned16(hits)) {
+    set_error("vf_trace: rays/hits must be non-null 16-byte aligned device pointers");
+    return VF_ERR_INVALID_ARG;
+  }
+  DeviceGuard g(h->device);
+  return launch_trace(h, rays, n, hits, trace_flags, (cudaStream_t)cuda_stream);
+}
+
+vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hit* host_hits, uint32_t trace_flags,
+                        void* cuda_stream) {
+  clear_error();
+  if (!h) {
+    set_error("vf_trace_host: null handle");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (n == 0) return VF_OK;
+  if (!host_rays || !host_hits) {
+    set_error("vf_trace_host: null buffer");
+    return VF_ERR_INVALID_ARG;
+  }
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const size_t rb = n * sizeof(vf_ray), hb = n * sizeof(vf_hit);
+  const size_t need = ((rb + 255) & ~(size_t)255) + hb;
+  if (h->stage_bytes < need) {
+    if (h->stage) cudaFree(h->stage);
+    h->stage = nullptr;
+    h->stage_bytes = 0;
+    cudaError_t e = cudaMalloc(&h->stage, need);
+    if (e != cudaSuccess) {
+      set_error("vf_trace_host: staging allocation of %zu bytes failed: %s", need, cudaGetErrorString(e));
+      return VF_ERR_OOM;
+    }
+    h->stage_bytes = need;
+  }
+  vf_ray* d_rays = (vf_ray*)h->stage;
+  vf_hit* d_hits = (vf_hit*)((char*)h->stage + ((rb + 255) & ~(size_t)255));
+  VF_CUDA_TRY(cudaMemcpyAsync(d_rays, host_rays, rb, cudaMemcpyHostToDevice, s));
+  vf_status st = launch_trace(h, d_rays, n, d_hits, trace_flags, s);
+  if (st != VF_OK) return st;
+  VF_CUDA_TRY(cudaMemcpyAsync(host_hits, d_hits, hb, cudaMemcpyDeviceToHost, s));
+  VF_CUDA_TRY(cudaStreamSynchronize(s));
+  return VF_OK;
+}
+
+vf_status vf_query(const vf_handle* h, const uint32_t* xyz, uint64_t n, uint32_t* rgba_out, void* cuda_stream) {
+  clear_error();
+  if (!h) {
+    set_error("vf_query: null handle");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (n == 0) return VF_OK;
+  if (!xyz || !rgba_out) {
+    set_error("vf_query: null buffer");
+    return VF_ERR_INVALID_ARG;
+  }
+  DeviceGuard g(h->device);
+  return launch_query(h, xyz, n, rgba_out, (cudaStream_t)cuda_stream);
+}
+
+vf_status vf_stats_get(const vf_handle* h, vf_stats* out) {
+  clear_error();
+  if (!h || !out) {
+    set_error("vf_stats_get: null argument");
+    return VF_ERR_INVALID_ARG;
+  }
+  *out = h->stats;
+  return VF_OK;
+}
+
+vf_status vf_buffer(const vf_handle* h, const uint32_t** words, uint64_t* n_words) {
+  clear_error();
+  if (!h || !words || !n_words) {
+    set_error("vf_buffer: null argument");
+    return VF_ERR_INVALID_ARG;
+  }
+  *words = h->buf;
+  *n_words = h->n_words;
+  return VF_OK;
+}
+
+vf_status vf_buffer_read(const vf_handle* h, uint64_t first, uint64_t count, uint32_t* host_out) {
+  clear_error();
+  if (!h || (!host_out && count)) {
+    set_error("vf_buffer_read: null argument");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (first > h->n_words || count > h->n_words - first) {
+    set_error("vf_buffer_read: range [%llu, +%llu) outside %llu words", (unsigned long long)first,
+              (unsigned long long)count, (unsigned long long)h->n_words);
+    return VF_ERR_INVALID_ARG;
+  }
+  if (!count) return VF_OK;
+  DeviceGuard g(h->device);
+  VF_CUDA_TRY(cudaMemcpy(host_out, h->buf + first, count * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return VF_OK;
+}
+
+void vf_destroy(vf_handle* h) {
+  if (!h) return;
+  DeviceGuard g(h->device);
+  if (h->buf) cudaFree(h->buf);
+  if (h->stage) cudaFree(h->stage);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,524 @@
+// trace.cu — the hot path: first-hit primary-ray intersection through a hybrid format.
+//
+// One thread per ray (north_star). The paper's generated intersection code is one function
+// per level (§4.2; fig:function_proto PAPER.md:182-186):
+//     intersect(node_id, ray, low):
+//       for child in ordered_hit_children(node_id, ray):
+//         if child and next_intersect(child, ray, low + child.pos): return True
+//       return False
+// with Raw levels walked by a branchless Amanatides-Woo DDA, SVO / SVDAG
+// levels by a pre-order traversal with a per-thread stack or, with
+// "restarting sparse voxel intersection", from the sub-volume root for every lookup
+// (PAPER.md:215), a unit function for single voxels and a root function that reads word 0
+// and tests the root box.
+//
+// B200 design (not a translation of the GLSL): the recursion is flattened into ONE loop over a
+// per-thread tier index, so lanes of a warp that sit at different levels still execute the
+// same instruction stream; each tier's kind-specific work is one `switch` arm instantiated only
+// for the base formats present (template parameter KINDS, the compile-time composition of the
+// level templates). Per-tier geometry is packed into 64-bit fields of TraceParams and
+// extracted with shifts (no indexed memory). Node headers are fetched with one vector load
+// (SVO: LDG.64, N^3-tree: LDG.128); inside an SVO / SVDAG / N^3 node, empty cells cost no
+// memory access (the occupancy mask stays in registers).
+//
+// Exactness (SURVEY.md §8(c) "How the GPU matches it"): the DDA never accumulates t. Every plane
+// event time is recomputed as  T^ = fl(fl(P - o_a) * inv_a),  inv_a = RN(1/d_a), |T^-T| <= ~3u|T|.
+// Every ordering decision (next axis to step, ties, entry cell, descent child, t_end) compares
+// two events with a certified fp32 test (gap > 2^-20 * max) and, if that fails, an exact fp64
+// fallback (P - o is exact in fp64 in the canonical domain; products use FMA TwoProduct).
+// The current time is carried as an EVENT {axis, plane} (or tmin) so the exact fallback can
+// always reconstruct it. The finest-voxel coordinate V of the current cell is kept exactly;
+// after a step at a coarse tier the sub-cell bits of the non-stepped axes are "stale" and are
+// re-derived (certified) only when the traversal descends at that event. Hence the hierarchy
+// visits exactly the cells of the flat right-limit walk (the oracle's definition) and
+// returns the same voxel, bit for bit.
+#include <stdint.h>
+
+#include "vf_internal.cuh"
+
+namespace vf {
+namespace {
+
+constexpr float kCertEps = 0x1p-20f;  // certification margin (>= 8u with u = 2^-24; see header)
+constexpr int TMIN_AXIS = 3;
+
+struct Ray {
+  float o[3], d[3], inv[3];
+  float tmin, tmax;
+};
+
+struct Event {
+  int axis;  // 0..2 plane event on that axis; TMIN_AXIS = tmin (start of the segment)
+  int P;     // plane coordinate in voxels (integer)
+  float t;   // fl(fl(P - o) * inv)  (or tmin)
+};
+
+__device__ __forceinline__ float tplane(int P, float o, float inv) { return __fmul_rn(__fsub_rn((float)P, o), inv); }
+
+// ---- exact fallbacks (rare; kept out of line) -------------------------------------------
+// sign(T_a(P) - T_b(Q)) for d_a, d_b != 0, exactly.
+__device__ __noinline__ int cmp_pp_exact(int P, float oa, float da, int Q, float ob, float db) {
+  const double A = (double)P - (double)oa;  // exact (<= 52 significant bits in the domain)
+  const double B = (double)Q - (double)ob;
+  const double x = A * (double)db, xe = fma(A, (double)db, -x);  // TwoProduct: A*db = x + xe
+  const double y = B * (double)da, ye = fma(B, (double)da, -y);
+  int s = (x > y) - (x < y);
+  if (s == 0) s = (xe > ye) - (xe < ye);
+  return ((da > 0.f) == (db > 0.f)) ? s : -s;  // T1 - T2 = (A db - B da) / (da db)
+}
+// sign(T_a(P) - s) for a scalar time s (tmin / tmax), exactly.
+__device__ __noinline__ int cmp_ps_exact(int P, float oa, float da, float s) {
+  const double A = (double)P - (double)oa;
+  const double S = (double)s * (double)da;  // 24 x 24 bits: exact
+  int r = (A > S) - (A < S);
+  return da > 0.f ? r : -r;  // T - s = (A - s da) / da
+}
+
+__device__ __forceinline__ int cert(float t1, float t2) {
+  const float df = t1 - t2;
+  const float m = fmaxf(fabsf(t1), fabsf(t2)) * kCertEps;
+  if (fabsf(df) > m) return df > 0.f ? 1 : -1;
+  return 2;
+}
+
+// sign(T_a(P) - T_b(Q)); t1 / t2 are the fp32 event values.
+__device__ __forceinline__ int cmp_pp(const Ray& r, int a, int P, float t1, int b, int Q, float t2) {
+  if (a == b) {
+    const int s = (P > Q) - (P < Q);
+    return r.d[a] > 0.f ? s : -s;
+  }
+  const int c = cert(t1, t2);
+  if (c != 2) return c;
+  return cmp_pp_exact(P, r.o[a], r.d[a], Q, r.o[b], r.d[b]);
+}
+
+// sign(E - T_b(Q)) for an event E (plane or tmin).
+__device__ __forceinline__ int cmp_ep(const Ray& r, const Event& E, int b, int Q) {
+  const float tq = tplane(Q, r.o[b], r.inv[b]);
+  if (E.axis == TMIN_AXIS) {
+    const int c = cert(E.t, tq);
+    if (c != 2) return c;
+    return -cmp_ps_exact(Q, r.o[b], r.d[b], E.t);
+  }
+  return cmp_pp(r, E.axis, E.P, E.t, b, Q, tq);
+}
+
+// sign(E1 - E2) for two events.
+__device__ __forceinline__ int cmp_ee(const Ray& r, const Event& E1, const Event& E2) {
+  if (E2.axis == TMIN_AXIS) {
+    if (E1.axis == TMIN_AXIS) return 0;
+    const int c = cert(E1.t, E2.t);
+    if (c != 2) return c;
+    return cmp_ps_exact(E1.P, r.o[E1.axis], r.d[E1.axis], E2.t);
+  }
+  return cmp_ep(r, E1, E2.axis, E2.P);
+}
+
+// sign(E - s) for a scalar s (tmax).
+__device__ __forceinline__ int cmp_es(const Ray& r, const Event& E, float s) {
+  if (E.axis == TMIN_AXIS) return (E.t > s) - (E.t < s);
+  const int c = cert(E.t, s);
+  if (c != 2) return c;
+  return cmp_ps_exact(E.P, r.o[E.axis], r.d[E.axis], s);
+}
+
+// Finest cell index on axis b at event E (right limit), known to lie in [lo, hi]:
+//   d_b > 0: T_b(k) <= E < T_b(k+1);   d_b < 0: T_b(k+1) <= E < T_b(k).
+// Candidate from fp32, then certified corrections (planes lo / hi+1 are known crossed /
+// not crossed and are never compared).
+__device__ __noinline__ int locate(const Ray& r, const Event& E, int b, int lo, int hi) {
+  const float x = fmaf(E.t, r.d[b], r.o[b]);
+  float kf = r.d[b] > 0.f ? floorf(x) : ceilf(x) - 1.0f;
+  kf = fminf(fmaxf(kf, (float)lo), (float)hi);
+  int k = (int)kf;
+  if (r.d[b] > 0.f) {
+    for (;;) {
+      if (k > lo && cmp_ep(r, E, b, k) < 0) {
+        --k;
+        continue;
+      }
+      if (k < hi && cmp_ep(r, E, b, k + 1) >= 0) {
+        ++k;
+        continue;
+      }
+      break;
+    }
+  } else {
+    for (;;) {
+      if (k < hi && cmp_ep(r, E, b, k + 1) < 0) {
+        ++k;
+        continue;
+      }
+      if (k > lo && cmp_ep(r, E, b, k) >= 0) {
+        --k;
+        continue;
+      }
+      break;
+    }
+  }
+  return k;
+}
+
+// Exact argmin of the three next-plane events (ties step together). c = candidate mask.
+__device__ __noinline__ int argmin_exact(const Ray& r, const int P[3], const float t[3], int c) {
+  int best = __ffs(c) - 1;
+  int set = 1 << best;
+  for (int a = best + 1; a < 3; ++a) {
+    if (!((c >> a) & 1)) continue;
+    const int s = cmp_pp(r, a, P[a], t[a], best, P[best], t[best]);
+    if (s < 0) {
+      best = a;
+      set = 1 << a;
+    } else if (s == 0) {
+      set |= 1 << a;
+    }
+  }
+  return set | (best << 4);
+}
+
+__device__ __forceinline__ uint32_t field4(uint64_t pack, uint32_t i) { return (uint32_t)(pack >> (4 * i)) & 15u; }
+
+template <uint32_t KINDS>
+__device__ __forceinline__ bool has_kind(uint32_t k) {
+  return (KINDS >> k) & 1u;
+}
+
+// Node header registers for the current tier.
+struct Header {
+  uint64_t mask;  // SVO/SVDAG: valid bits; N^3: 64-bit occupancy
+  uint32_t base;  // SVO: first child; SVDAG: node address; N^3: children block
+};
+
+template <uint32_t KINDS>
+__device__ __forceinline__ Header load_header(const uint32_t* __restrict__ buf, uint32_t kind, uint32_t N) {
+  Header h;
+  h.mask = 0;
+  h.base = N;
+  if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(buf + N));
+    h.base = v.x;
+    h.mask = v.y & 0xFFu;
+  } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
+    h.mask = __ldg(buf + N) & 0xFFu;
+  } else if (has_kind<KINDS>(K_NTREE) && kind == K_NTREE) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(buf + N));
+    h.mask = (uint64_t)v.x | ((uint64_t)v.y << 32);
+    h.base = v.z;
+  }
+  return h;
+}
+
+template <uint32_t KINDS, bool RESTART>
+__global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
+                                                    const float4* __restrict__ rays, int4* __restrict__ hits,
+                                                    uint64_t n) {
+  const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (gid >= n) return;
+  const float4 r0 = __ldg(rays + 2 * gid), r1 = __ldg(rays + 2 * gid + 1);
+  int4 out = make_int4(-1, -1, -1, __float_as_int(__int_as_float(0x7f800000)));
+  Ray r;
+  r.o[0] = r0.x;
+  r.o[1] = r0.y;
+  r.o[2] = r0.z;
+  r.tmin = r0.w;
+  r.d[0] = r1.x;
+  r.d[1] = r1.y;
+  r.d[2] = r1.z;
+  r.tmax = r1.w;
+  const bool tmax_finite = r.tmax < __int_as_float(0x7f800000);
+  const int R[3] = {p.dims[0], p.dims[1], p.dims[2]};
+
+  do {
+    // ---- root function: word 0, root-box test ---------------------------
+    if (p.root == 0) break;  // empty volume: buffer [0]
+    int moving = 0;
+    for (int a = 0; a < 3; ++a) {
+      if (r.d[a] != 0.f) moving |= 1 << a;
+      r.inv[a] = r.d[a] != 0.f ? __frcp_rn(r.d[a]) : 0.f;
+    }
+    if (!moving) break;                        // reading A5: all-zero direction misses
+    if (!(r.tmin < r.tmax) && tmax_finite) break;
+    Event E{TMIN_AXIS, 0, r.tmin};
+    bool miss = false;
+    for (int a = 0; a < 3; ++a) {
+      if (!((moving >> a) & 1)) {
+        // half-open membership: floor(o_a) in [0, R_a)
+        if (!(r.o[a] >= 0.f && r.o[a] < (float)R[a])) miss = true;
+        continue;
+      }
+      const int Pe = r.d[a] > 0.f ? 0 : R[a];
+      const Event Ea{a, Pe, tplane(Pe, r.o[a], r.inv[a])};
+      if (cmp_ee(r, Ea, E) > 0) E = Ea;
+    }
+    if (miss) break;
+    for (int a = 0; a < 3 && !miss; ++a) {
+      if (!((moving >> a) & 1)) continue;
+      const int Px = r.d[a] > 0.f ? R[a] : 0;
+      if (cmp_ep(r, E, a, Px) >= 0) miss = true;  // entered at / after the exit of slab a
+    }
+    if (miss || (tmax_finite && cmp_es(r, E, r.tmax) >= 0)) break;
+
+    // ---- entry cell (exact right limit at t_start) -------------------------------------
+    int V[3];
+    for (int b = 0; b < 3; ++b) V[b] = ((moving >> b) & 1) ? locate(r, E, b, 0, R[b] - 1) : (int)floorf(r.o[b]);
+
+    // ---- flattened per-level traversal ---------------------------------------------------
+    const int T = (int)p.n_tiers;
+    int t = 0;
+    uint32_t N = p.root;
+    uint32_t stk[VF_MAX_TIERS];
+    uint32_t kind = p.kind_pack & 3u;
+    Header hd = load_header<KINDS>(buf, kind, N);
+    int stale = 0;
+    bool hit = false;
+    // Invariant at the top of the loop: V >> lc(t) is the current (untested) cell of node N
+    // at tier t, entered at event E. A pop always follows a step, so it lands on a new cell.
+    for (;;) {
+      const uint32_t lc = field4(p.lc_pack, t);
+      {
+        // -- test the current cell of the current node (ordered_hit_children, one child)
+        const uint32_t lf = field4(p.lf_pack, t);
+        const uint32_t msk = t == 0 ? 0xFFFFFFFFu : ((1u << lf) - 1u);
+        const uint32_t lx = ((uint32_t)V[0] >> lc) & msk, ly = ((uint32_t)V[1] >> lc) & msk,
+                       lz = ((uint32_t)V[2] >> lc) & msk;
+        const uint32_t sx = t == 0 ? p.lf0[0] : lf, sxy = t == 0 ? p.lf0[0] + p.lf0[1] : 2 * lf;
+        const bool last = (p.last_mask >> t) & 1u;
+        const bool finest = t == T - 1;
+        bool occ = false;
+        uint32_t child = 0;
+        if (has_kind<KINDS>(K_RAW) && kind == K_RAW) {
+          // 64-bit index: a single-level R(11^3) grid has 2^33 cells (reading A15)
+          const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
+          child = __ldg(buf + (size_t)N + lin);
+          occ = child != 0u;
+        } else {
+          const uint32_t lin = lx + (ly << sx) + (lz << sxy);
+          occ = (hd.mask >> lin) & 1u;
+          if (occ && !finest) {
+            const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
+            if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
+              child = hd.base + 2u * rank;
+            } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
+              child = __ldg(buf + hd.base + 1u + rank);
+            } else {
+              child = hd.base + (last ? 1u : 4u) * rank;
+            }
+            if (last) child = __ldg(buf + child);  // leaf TermInt -> next level's root
+          }
+        }
+        if (occ) {
+          if (finest) {  // unit intersection
+            hit = true;
+            break;
+          }
+          // descend at event E: make the sub-cell bits of stale axes exact
+          if (stale) {
+            for (int b = 0; b < 3; ++b)
+              if ((stale >> b) & 1) {
+                const int lo = (V[b] >> lc) << lc;
+                V[b] = locate(r, E, b, lo, lo + (1 << lc) - 1);
+              }
+            stale = 0;
+          }
+          if (!RESTART || ((p.top_mask >> t) & 1u) || kind == K_RAW) stk[t] = N;
+          ++t;
+          N = child;
+          kind = (p.kind_pack >> (2 * t)) & 3u;
+          hd = load_header<KINDS>(buf, kind, N);
+          continue;
+        }
+      }
+      // -- step: exact next event among the three axes at this tier's cell size
+      int Pn[3];
+      float tn[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int c = V[a] >> lc;
+        Pn[a] = (r.d[a] > 0.f ? c + 1 : c) << lc;
+        tn[a] = ((moving >> a) & 1) ? tplane(Pn[a], r.o[a], r.inv[a]) : __int_as_float(0x7f800000);
+      }
+      const float m = fminf(fminf(tn[0], tn[1]), tn[2]);
+      const float thr = fmaf(m, kCertEps, m);
+      const int c = (tn[0] <= thr ? 1 : 0) | (tn[1] <= thr ? 2 : 0) | (tn[2] <= thr ? 4 : 0);
+      int S, a0;
+      if ((c & (c - 1)) == 0) {
+        S = c;
+        a0 = __ffs(c) - 1;
+      } else {
+        const int res = argmin_exact(r, Pn, tn, c);
+        S = res & 7;
+        a0 = res >> 4;
+      }
+      E.axis = a0;
+      E.P = Pn[a0];
+      E.t = tn[a0];
+      if (tmax_finite && cmp_es(r, E, r.tmax) >= 0) break;  // segment ends (reading A7)
+      uint32_t h = 0;
+      bool out_of_box = false;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (!((S >> a) & 1)) continue;
+        const int nv = r.d[a] > 0.f ? Pn[a] : Pn[a] - 1;
+        if (nv < 0 || nv >= R[a]) out_of_box = true;
+        h = max(h, 31u - __clz((uint32_t)(nv ^ V[a])));
+        V[a] = nv;
+      }
+      if (out_of_box) break;  // left the root box: miss
+      if (lc) stale |= ~S & moving;
+      stale &= ~S;
+      const int tau = (int)field4(p.tau_pack, h);
+      if (tau < t) {
+        // left the current node: pop (stack) or restart from the level root
+        if (!RESTART) {
+          t = tau;
+          N = stk[t];
+          kind = (p.kind_pack >> (2 * t)) & 3u;
+          hd = load_header<KINDS>(buf, kind, N);
+        } else {
+          const int top = (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tau);
+          t = top;
+          N = stk[t];
+          kind = (p.kind_pack >> (2 * t)) & 3u;
+          hd = load_header<KINDS>(buf, kind, N);
+          while (t < tau) {  // re-descend through nodes that contain the current cell
+            const uint32_t lct = field4(p.lc_pack, t), lf = field4(p.lf_pack, t);
+            const uint32_t msk = t == 0 ? 0xFFFFFFFFu : ((1u << lf) - 1u);
+            const uint32_t lin = (((uint32_t)V[0] >> lct) & msk) + ((((uint32_t)V[1] >> lct) & msk) << (t == 0 ? p.lf0[0] : lf)) +
+                                 ((((uint32_t)V[2] >> lct) & msk) << (t == 0 ? p.lf0[0] + p.lf0[1] : 2 * lf));
+            const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
+            uint32_t child;
+            if (has_kind<KINDS>(K_SVO) && kind == K_SVO)
+              child = hd.base + 2u * rank;
+            else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG)
+              child = __ldg(buf + hd.base + 1u + rank);
+            else
+              child = hd.base + 4u * rank;  // N^3 internal (t < tau <= last tier of the level)
+            ++t;
+            N = child;
+            kind = (p.kind_pack >> (2 * t)) & 3u;
+            hd = load_header<KINDS>(buf, kind, N);
+          }
+        }
+      }
+    }
+    if (hit) out = make_int4(V[0], V[1], V[2], __float_as_int(E.t));
+  } while (0);
+  hits[gid] = out;
+}
+
+// ---- point query: integer-only descent (test aid) ------------------------------------------
+__global__ void query_kernel(const TraceParams p, const uint32_t* __restrict__ buf, const uint32_t* __restrict__ xyz,
+                             uint32_t* __restrict__ out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t V[3] = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
+    uint32_t res = 0;
+    if (p.root != 0 && V[0] < (uint32_t)p.dims[0] && V[1] < (uint32_t)p.dims[1] && V[2] < (uint32_t)p.dims[2]) {
+      uint32_t N = p.root;
+      for (uint32_t t = 0; t < p.n_tiers; ++t) {
+        const uint32_t kind = (p.kind_pack >> (2 * t)) & 3u;
+        const uint32_t lc = field4(p.lc_pack, t), lf = field4(p.lf_pack, t);
+        const uint32_t msk = t == 0 ? 0xFFFFFFFFu : ((1u << lf) - 1u);
+        const uint32_t lin = ((V[0] >> lc) & msk) + (((V[1] >> lc) & msk) << (t == 0 ? p.lf0[0] : lf)) +
+                             (((V[2] >> lc) & msk) << (t == 0 ? p.lf0[0] + p.lf0[1] : 2 * lf));
+        const bool last = (p.last_mask >> t) & 1u;
+        uint32_t word;
+        if (kind == K_RAW) {
+          word = buf[(size_t)N + lin];
+        } else {
+          uint64_t mask;
+          uint32_t base;
+          if (kind == K_SVO) {
+            base = buf[N];
+            mask = buf[N + 1] & 0xFFu;
+          } else if (kind == K_SVDAG) {
+            base = N;
+            mask = buf[N] & 0xFFu;
+          } else {
+            mask = (uint64_t)buf[N] | ((uint64_t)buf[N + 1] << 32);
+            base = buf[N + 2];
+          }
+          if (!((mask >> lin) & 1u)) {
+            word = 0;
+          } else {
+            const uint32_t rank = __popcll(mask & ((1ull << lin) - 1ull));
+            uint32_t c;
+            if (kind == K_SVO)
+              c = base + 2u * rank;
+            else if (kind == K_SVDAG)
+              c = buf[base + 1u + rank];
+            else
+              c = base + (last ? 1u : 4u) * rank;
+            word = last ? buf[c] : c;
+          }
+        }
+        if (word == 0) {
+          res = 0;
+          break;
+        }
+        res = word;
+        N = word;
+      }
+    }
+    out[i] = res;
+  }
+}
+
+using KernelFn = void (*)(const TraceParams, const uint32_t*, const float4*, int4*, uint64_t);
+
+template <uint32_t K>
+struct Table {
+  static KernelFn get(bool restart) { return restart ? trace_kernel<K, true> : trace_kernel<K, false>; }
+};
+
+KernelFn select_kernel(uint32_t kinds, bool restart) {
+  switch (kinds) {
+#define VF_CASE(k) \
+  case k: return Table<k>::get(restart);
+    VF_CASE(1) VF_CASE(2) VF_CASE(3) VF_CASE(4) VF_CASE(5) VF_CASE(6) VF_CASE(7) VF_CASE(8) VF_CASE(9) VF_CASE(10)
+    VF_CASE(11) VF_CASE(12) VF_CASE(13) VF_CASE(14) VF_CASE(15)
+#undef VF_CASE
+    default: return nullptr;
+  }
+}
+
+}  // namespace
+
+vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags, cudaStream_t s) {
+  if (n == 0) return VF_OK;
+  uint32_t kinds = 0;
+  for (uint32_t t = 0; t < h->fmt.n_tiers; ++t) kinds |= 1u << h->fmt.tiers[t].kind;
+  KernelFn fn = select_kernel(kinds, (flags & VF_TRACE_RESTART_SV) != 0);
+  if (!fn) {
+    set_error("vf_trace: no kernel instantiated for kind set 0x%x", kinds);
+    return VF_ERR_UNSUPPORTED;
+  }
+  const unsigned threads = 256;
+  const uint64_t blocks = (n + threads - 1) / threads;
+  if (blocks > 0x7fffffffull) {
+    set_error("vf_trace: %llu rays exceed one launch", (unsigned long long)n);
+    return VF_ERR_INVALID_ARG;
+  }
+  fn<<<(unsigned)blocks, threads, 0, s>>>(h->tp, h->buf, reinterpret_cast<const float4*>(rays),
+                                          reinterpret_cast<int4*>(hits), n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("vf_trace: launch failed: %s", cudaGetErrorString(e));
+    return VF_ERR_CUDA;
+  }
+  return VF_OK;
+}
+
+vf_status launch_query(const Handle* h, const uint32_t* xyz, uint64_t n, uint32_t* out, cudaStream_t s) {
+  if (n == 0) return VF_OK;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  query_kernel<<<(unsigned)blocks, 256, 0, s>>>(h->tp, h->buf, xyz, out, n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("vf_query: launch failed: %s", cudaGetErrorString(e));
+    return VF_ERR_CUDA;
+  }
+  return VF_OK;
+}
+
+}  // namespace vf

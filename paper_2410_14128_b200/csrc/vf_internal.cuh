@@ -1,0 +1,99 @@
+// vf_internal.cuh — shared internals of libvf.so (format tiers, handle, errors).
+//
+// A hybrid format (§3.2) is expanded into TIERS, one per node level:
+//   Raw R(w,h,d)        -> 1 tier, fan-out 2^w x 2^h x 2^d
+//   SVO S(L) / SVDAG G(L) -> L tiers, fan-out 2 x 2 x 2
+//   N^3-tree T(n,d)      -> d tiers, fan-out 2^n per axis     (layout SURVEY A13)
+// Tier 0 is the root. lc(t) = log2 of a tier-t cell's edge in voxels (cubic for every tier,
+// since every level but the first is cubic). A tier's "cells" are the
+// children of its nodes; the cells of a level's last tier are that level's sub-volumes
+// (terminating integers), and the cells of the last tier overall are voxels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/vf.h"
+
+namespace vf {
+
+enum TierKind : uint32_t { K_RAW = 0, K_SVO = 1, K_SVDAG = 2, K_NTREE = 3 };
+
+struct Tier {
+  uint32_t kind;   // TierKind
+  uint32_t lf[3];  // log2 fan-out per axis (cubic except possibly tier 0)
+  uint32_t lc;     // log2 cell size in voxels
+  uint32_t level;  // index of the level this tier belongs to
+  uint32_t depth;  // depth within its level (0 = level top)
+  bool top;        // first tier of its level (its node is the level's sub-volume root)
+  bool last;       // last tier of its level (its cells are terminating integers)
+};
+
+struct Format {
+  uint32_t n_levels = 0;
+  vf_level levels[VF_MAX_LEVELS];
+  uint32_t n_tiers = 0;
+  Tier tiers[VF_MAX_TIERS];
+  uint32_t dims[3] = {0, 0, 0};
+};
+
+// Packed per-tier parameters passed to the trace / query kernels by value (all uniform).
+// Fields for tier t are extracted with shifts, so a lane at any tier reads them from
+// registers / the constant bank without indexed memory.
+struct TraceParams {
+  uint64_t lc_pack;     // 4 bits per tier: lc(t)
+  uint64_t lf_pack;     // 4 bits per tier: cubic log2 fan-out (tier 0: x)
+  uint64_t tau_pack;    // 4 bits per h in [0,15]: deepest tier whose node contains both cells
+                        // whose coordinates first differ at bit h
+  uint32_t kind_pack;   // 2 bits per tier
+  uint32_t top_mask;    // bit t: tier t is its level's top
+  uint32_t last_mask;   // bit t: tier t is its level's last tier
+  uint32_t top_of;      // unused (reserved)
+  uint32_t lf0[3];      // tier-0 fan-out per axis (log2)
+  int32_t dims[3];      // resolution per axis
+  uint32_t n_tiers;
+  uint32_t root;        // word 0 (root pointer); 0 => empty volume
+  uint32_t level_top_pack_lo;  // 4 bits per tier: tier index of its level's top (tiers 0..7)
+  uint32_t level_top_pack_hi;  // tiers 8..15
+};
+
+struct Handle {
+  int device = 0;
+  Format fmt;
+  TraceParams tp;
+  uint32_t* buf = nullptr;  // device words
+  uint64_t n_words = 0;
+  vf_stats stats{};
+  // staging for vf_trace_host
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+// errors
+void set_error(const char* fmt, ...);
+void clear_error();
+
+// format.cu
+vf_status expand_format(const vf_level* levels, uint32_t n, Format* out);
+TraceParams make_trace_params(const Format& f, uint32_t root);
+
+// build.cu
+vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cudaStream_t s, Handle* h);
+
+// trace.cu
+vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags,
+                       cudaStream_t s);
+vf_status launch_query(const Handle* h, const uint32_t* xyz, uint64_t n, uint32_t* out, cudaStream_t s);
+
+#define VF_CUDA_TRY(expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess) {                                                                \
+      ::vf::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return _e == cudaErrorMemoryAllocation ? VF_ERR_OOM : VF_ERR_CUDA;                    \
+    }                                                                                       \
+  } while (0)
+
+}  // namespace vf

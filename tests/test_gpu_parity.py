@@ -1,0 +1,198 @@
+"""GPU parity: the CUDA path through the C ABI (libvf.so) vs the CPU oracle, element by element.
+
+Every hybrid format must return the oracle's first-hit voxel bit for bit and the miss flag
+exactly, t within 1e-4 relative (north_star). Volumes and rays are the
+seeded synthetic inputs of inputs/ (SURVEY.md §8(d)); the oracle never sees GPU output.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+from inputs import rays as R
+from parity import assert_parity, gpu_trace
+
+pytestmark = pytest.mark.gpu
+
+
+def _vf():
+    from paper_2410_14128_b200 import vf
+    return vf
+
+
+def _dense_dev(d):
+    import torch
+    return torch.from_numpy(inputs.dense_host(d).view(np.int32)).cuda()
+
+
+def _rays_small(dims, seed, n_adv=3000, n_rand=2000):
+    return np.concatenate([R.adversarial_rays(n_adv, dims, seed), R.random_rays(n_rand, dims, seed + 1)])
+
+
+# ---------------------------------------------------------------- cfg1: Raw single level
+def test_cfg1_sphere_raw():
+    vf = _vf()
+    d = inputs.sphere(64, 28)
+    h = vf.build(_dense_dev(d), "R(6, 6, 6)")
+    g = oracle.Grid.from_generator(d)
+    ortho, _ = R.ortho(256, 256, 0.25, -1.0)
+    obl, _ = R.ortho(256, 256, 0.25, -1.0, direction=(0.25, 0.5, 1.0))
+    for name, rays in [("ortho", ortho), ("oblique", obl), ("adversarial", _rays_small((64,) * 3, 5))]:
+        ref = g.trace(rays)
+        for restart in (False, True):
+            xyz, t = gpu_trace(h, rays, restart)
+            assert_parity(xyz, t, ref, f"cfg1 {name} restart={restart}")
+    s = h.stats()
+    assert s["nonempty_voxels"] == 92096 and s["bytes_used"] == 4 * (4 + 64 ** 3)
+
+
+# ---------------------------------------------------------------- many formats, small volumes
+SMALL_FORMATS_16 = [
+    "R(4, 4, 4)", "S(4)", "G(4)", "T(2, 2)", "T(1, 4)", "R(2^3) G(2)", "R(1^3) S(3)", "G(2) R(2^3)",
+    "S(2) R(2, 2, 2)", "T(2, 1) R(2^3)", "T(2, 1) T(1, 1) R(1^3)", "R(1, 1, 1) T(2, 1) S(1)",
+    "R(1^3) S(1) G(1) T(1, 1)", "G(1) T(2, 1) R(1^3)", "R(2^3) R(2^3)", "S(1) S(1) S(1) S(1)",
+    "G(3) G(1)", "T(2, 1) T(2, 1)",
+]
+
+
+@pytest.mark.parametrize("fmt", SMALL_FORMATS_16)
+@pytest.mark.parametrize("p", [0.03, 0.3])
+def test_small_formats_vs_oracle(fmt, p):
+    vf = _vf()
+    dims = (16, 16, 16)
+    d = inputs.random_occupancy(dims, p, 1234 + int(p * 100))
+    h = vf.build(_dense_dev(d), fmt)
+    rays = _rays_small(dims, 99)
+    ref = oracle.Grid.from_generator(d).trace(rays)
+    for restart in (False, True):
+        xyz, t = gpu_trace(h, rays, restart)
+        assert_parity(xyz, t, ref, f"{fmt} p={p} restart={restart}")
+
+
+@pytest.mark.parametrize("fmt,dims", [
+    ("R(2, 1, 3) G(2)", (16, 8, 32)), ("R(0, 2, 1) S(3)", (8, 32, 16)), ("R(3, 0, 1) T(2, 1) R(1^3)", (64, 8, 16)),
+    ("R(1, 2, 0) R(2^3)", (8, 16, 4)),
+])
+def test_noncubic_first_level(fmt, dims):
+    vf = _vf()
+    d = inputs.random_occupancy(dims, 0.1, 77)
+    h = vf.build(_dense_dev(d), fmt)
+    rays = _rays_small(dims, 7)
+    ref = oracle.Grid.from_generator(d).trace(rays)
+    for restart in (False, True):
+        xyz, t = gpu_trace(h, rays, restart)
+        assert_parity(xyz, t, ref, f"{fmt} restart={restart}")
+
+
+# ---------------------------------------------------------------- cfg2: 256^3 Menger
+CFG2_FORMATS = ["S(8)", "G(8)", "G(5) R(3, 3, 3)", "T(2, 4)", "R(8, 8, 8)", "R(3^3) G(5)"]
+
+
+@pytest.mark.parametrize("fmt", CFG2_FORMATS)
+def test_cfg2_menger(fmt):
+    import torch
+    vf = _vf()
+    d = inputs.menger(256, 5)
+    keys, rgba = inputs.voxels_device(d)
+    h = vf.build((keys, rgba, (256, 256, 256)), fmt)
+    g = oracle.Grid.from_generator(d)
+    persp, _ = R.camera("menger", scale=4)        # 256 x 256 subsample of the 1024^2 camera
+    tunnel, _ = R.camera("menger_tunnel", scale=8)
+    n = 3 ** 5
+    ys, xs = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    ax = R.pack(np.stack([xs.ravel() + 0.5, ys.ravel() + 0.5, np.full(n * n, -2.0)], 1), np.array([[0, 0, 1.0]]))
+    for name, rays in [("persp", persp), ("tunnel", tunnel), ("axis", ax), ("adv", _rays_small((256,) * 3, 3, 2000, 1000))]:
+        ref = g.trace(rays)
+        for restart in (False, True):
+            xyz, t = gpu_trace(h, rays, restart)
+            assert_parity(xyz, t, ref, f"cfg2 {fmt} {name} restart={restart}")
+    assert h.stats()["nonempty_voxels"] == 20 ** 5
+    del torch
+
+
+# ---------------------------------------------------------------- build: query / sizes
+@pytest.mark.parametrize("fmt", ["R(4, 4, 4)", "S(4)", "G(4)", "T(2, 2)", "R(2^3) G(2)", "G(1) T(2, 1) R(1^3)",
+                                 "R(1^3) S(1) G(1) T(1, 1)"])
+def test_query_equals_dense(fmt):
+    import torch
+    vf = _vf()
+    dims = (16, 16, 16)
+    d = inputs.random_occupancy(dims, 0.2, 5)
+    dense = inputs.dense_host(d)
+    h = vf.build(torch.from_numpy(dense.view(np.int32)).cuda(), fmt)
+    zz, yy, xx = np.meshgrid(np.arange(16), np.arange(16), np.arange(16), indexing="ij")
+    xyz = torch.from_numpy(np.stack([xx.ravel(), yy.ravel(), zz.ravel()], 1).astype(np.int32)).cuda()
+    got = h.query(xyz).cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(got, dense.ravel())
+
+
+def test_size_closed_forms():
+    """SURVEY.md §8(c) c-3 'Bytes' row (paper layout, word 0 included)."""
+    import torch
+    vf = _vf()
+
+    def words(fmt, d, flags=vf.VF_BUILD_DEFAULT):
+        h = vf.build(torch.from_numpy(inputs.dense_host(d).view(np.int32)).cuda(), fmt, flags)
+        return h.stats()["paper_layout_bytes"] // 4
+
+    L = 4
+    R_ = 2 ** L
+    solid = inputs.solid((R_,) * 3)
+    one = inputs.single((R_,) * 3, (3, 9, 14))
+    empty = inputs.empty((R_,) * 3)
+    assert words(f"S({L})", empty) == 1 and words(f"G({L})", empty) == 1   # buffer [0]
+    assert words(f"S({L})", solid) == 1 + 2 * (8 ** (L + 1) - 1) // 7
+    assert words(f"G({L})", solid) == 1 + 9 * L + 1                          # L internal + 1 leaf
+    assert words(f"S({L})", one) == 1 + 2 * (L + 1)
+    assert words(f"G({L})", one) == 1 + 2 * L + 1
+    assert words("T(2, 2)", solid) == 1 + 4 * (64 ** 2 - 1) // 63 + 64 ** 2
+    assert words("T(2, 2)", one) == 1 + 4 * 2 + 1
+    assert words(f"R({L}, {L}, {L})", one) == 1 + R_ ** 3
+    # whole-level dedup never adds storage
+    rnd = inputs.random_occupancy((R_,) * 3, 0.3, 9)
+    for fmt in ["R(2^3) G(2)", "R(1^3) G(3)", "G(2) G(2)"]:
+        assert words(fmt, rnd, vf.VF_BUILD_WHOLE_LEVEL_DEDUP) <= words(fmt, rnd, 0)
+
+
+def test_empty_volume_all_miss():
+    import torch
+    vf = _vf()
+    dims = (8, 8, 8)
+    for fmt in ["R(3, 3, 3)", "G(3)", "S(3)", "T(1, 3)", "R(1^3) G(2)"]:
+        h = vf.build(torch.zeros((8, 8, 8), dtype=torch.int32, device="cuda"), fmt)
+        assert h.stats()["root"] == 0 and h.bytes_used == 4
+        rays = _rays_small(dims, 1, 300, 300)
+        xyz, t = gpu_trace(h, rays)
+        assert (xyz == -1).all() and np.isinf(t).all()
+
+
+def test_format_errors():
+    import torch
+    vf = _vf()
+    v = torch.zeros((16, 16, 16), dtype=torch.int32, device="cuda")
+    with pytest.raises(vf.VfError) as e:
+        vf.build(v, "R(2, 2, 2) R(1, 2, 1)")
+    assert e.value.status == vf.VF_ERR_FORMAT
+    with pytest.raises(vf.VfError) as e:
+        vf.build(v, "D(2^3, 6) G(2)")
+    assert e.value.status == vf.VF_ERR_UNSUPPORTED
+    with pytest.raises(vf.VfError) as e:
+        vf.build(v, "G(5)")
+    assert e.value.status == vf.VF_ERR_FORMAT
+
+
+def test_trace_host_matches_device():
+    import torch
+    vf = _vf()
+    d = inputs.random_occupancy((32, 32, 32), 0.05, 3)
+    h = vf.build(_dense_dev(d), "R(2^3) G(3)")
+    rays = R.random_rays(5000, (32, 32, 32), 4)
+    xyz, t = gpu_trace(h, rays)
+    hr = torch.from_numpy(rays).pin_memory()
+    hh = torch.empty((len(rays), 4), dtype=torch.int32).pin_memory()
+    h.trace_host(hr, hh)
+    out = hh.numpy()
+    np.testing.assert_array_equal(out[:, :3], xyz)
+    np.testing.assert_array_equal(out[:, 3].view(np.float32), t)
