@@ -1,0 +1,437 @@
+#!/usr/bin/env python3
+"""bench.py — primary-ray Mrays/s through a hybrid voxel format on B200 (BASELINE.json metric).
+
+Default workload (N=1): cfg4 of BASELINE.json — the 2048^3 voxelised-synthetic city (TEX=1,
+inputs.city), 1920x1080 aerial perspective rays, format R(4^3) G(7) (the paper's always-Pareto
+2048^3 format). A step = one vf_trace of the whole frame (all §8(a) rows run inside
+the one trace kernel); inputs are resident in HBM; L2 (126 MB) is flushed between timed steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config cfg4] [--format "R(4^3) G(7)"] [--restart] [--sweep]
+
+Multi-GPU (torchrun, one rank per GPU): the volume is replicated, the frame's 16x16 screen tiles
+are interleaved across ranks (tile mod N), each rank traces its tiles, and the hit buffers are
+gathered to rank 0 with one NCCL collective (north_star). The frame is fixed: strong scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (volume preset, camera preset, default format, description)
+    "cfg1": ("sphere", None, "R(6, 6, 6)", "64^3 analytic sphere, Raw only, 256x256 orthographic rays"),
+    "cfg2": ("menger", "menger", "G(5) R(3, 3, 3)", "256^3 Menger sponge, 1024x1024 perspective rays"),
+    "cfg3": ("terrain", "terrain", "T(2, 2) T(2, 1) R(4, 4, 4)", "1024^3 noise terrain/caves, 1920x1080 rays"),
+    "cfg4": ("city", "city", "R(4, 4, 4) G(7)", "2048^3 synthetic city blocks, 1920x1080 aerial rays"),
+    "cfg5": ("sparse", "sparse", "R(4, 4, 4) G(8)", "4096^3 sparse shells, 3840x2160 rays"),
+}
+SWEEP = {
+    "cfg4": ["R(4, 4, 4) G(7)", "R(3, 3, 3) G(8)", "G(11)", "S(11)", "R(6, 6, 6) G(5)", "R(4, 4, 4) S(7)",
+             "R(1, 1, 1) T(2, 5)", "T(2, 4) R(3, 3, 3)", "R(4, 4, 4) R(4, 4, 4) R(3, 3, 3)", "R(8, 8, 8) G(3)"],
+}
+L2_BYTES = 126 * 2**20
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def make_volume(name):
+    import inputs
+    return {"sphere": inputs.sphere, "menger": inputs.menger, "terrain": inputs.terrain, "city": inputs.city,
+            "sparse": inputs.sparse}[name]()
+
+
+def make_rays(cfg):
+    from inputs import rays as R
+    vol, cam, _, _ = CONFIGS[cfg]
+    if cam is None:
+        return R.ortho(256, 256, 0.25, -1.0)
+    return R.camera(cam)
+
+
+def shard_tiles(width, height, perm, rank, world, tile=16):
+    """Indices (into the tile-ordered ray array) owned by `rank`: 16x16 screen tiles, tile mod N."""
+    px, py = perm % width, perm // width
+    tid = (py // tile) * ((width + tile - 1) // tile) + (px // tile)
+    return np.nonzero(tid % world == rank)[0]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/vf_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader",
+                                          "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1].split()[0]), float(f[2].split()[0]), f[4:]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for _, _, fl in rows:
+            for n, v in zip(names, fl[1:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        busy = [r[0] for r in rows if r[0] > 300] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(r[1] for r in rows), "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def peaks():
+    try:
+        return json.load(open(MEASURED_PEAKS))
+    except Exception:
+        return {}
+
+
+def cpu_baseline(vol_desc, rays, gpu_xyz, gpu_t, budget_s=12.0):
+    """Oracle (as it stands) on the box's host cores over a bounded, evenly strided sample of the
+    same frame; also checks parity of the sampled rays against the GPU hits."""
+    import oracle
+    from parity import compare
+    g = oracle.Grid.procedural(vol_desc) if vol_desc.gen != 5 else oracle.Grid.from_generator(vol_desc)
+    cores = oracle.max_threads()
+    n = len(rays)
+    m = min(n, 2048)
+    total_s, done, checked, bad = 0.0, 0, 0, 0
+    while True:
+        idx = np.linspace(0, n - 1, m).astype(np.int64)
+        t0 = time.perf_counter()
+        ref = g.trace(rays[idx])
+        dt = time.perf_counter() - t0
+        nb, _ = compare(gpu_xyz[idx], gpu_t[idx], ref)
+        checked, bad = m, nb
+        total_s, done = dt, m
+        if dt > budget_s / 4 or m >= n:
+            break
+        m = min(n, int(m * min(8.0, max(2.0, budget_s / max(dt, 1e-3) / 2))))
+    return {"value": done / total_s / 1e6, "unit": "Mrays/s", "cores": cores, "kind": "oracle",
+            "sample": f"{done} of {n} rays (evenly strided) of the same frame; exact int128 DDA over the "
+                      f"procedural occupancy (vg_voxel per visited cell), OpenMP {cores} threads; {total_s:.2f} s",
+            "parity_checked": checked, "parity_mismatches": bad}
+
+
+def counters_for(handle, rays_dev, restart):
+    return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import inputs
+    from paper_2410_14128_b200 import vf
+
+    cfg = args.config
+    vname, _, deffmt, desc = CONFIGS[cfg]
+    fmt = args.format or deffmt
+    vol = make_volume(vname)
+    t0 = time.perf_counter()
+    keys, rgba = inputs.voxels_device(vol)
+    dims = inputs.dims_of(vol)
+    handle = vf.build((keys, rgba, dims), fmt)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    nonempty = keys.shape[0]
+    del keys, rgba
+    torch.cuda.empty_cache()
+    stats = handle.stats()
+
+    rays_all, perm = make_rays(cfg)
+    W = int(perm.max() + 1)
+    width = {"cfg1": 256}.get(cfg, None)
+    from inputs.rays import CAMERAS
+    cam = CONFIGS[cfg][1]
+    width, height = (256, 256) if cam is None else (CAMERAS[cam]["width"], CAMERAS[cam]["height"])
+    own = shard_tiles(width, height, perm, rank, world) if world > 1 else np.arange(len(rays_all))
+    rays = torch.from_numpy(np.ascontiguousarray(rays_all[own])).to(dev)
+    n_local = rays.shape[0]
+    hits = torch.empty((n_local, 4), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+
+    # gather buffers (rank 0)
+    counts = [len(shard_tiles(width, height, perm, r, world)) for r in range(world)] if world > 1 else [n_local]
+
+    def step():
+        handle.trace(rays, hits, restart=args.restart)
+
+    def gather():
+        if world == 1:
+            return
+        if rank == 0:
+            bufs = [torch.empty((c, 4), dtype=torch.int32, device=dev) for c in counts]
+            dist.gather(hits, gather_list=bufs, dst=0)
+        else:
+            dist.gather(hits, dst=0)
+
+    for _ in range(args.warmup):
+        step()
+        gather()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kstarts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i)  # write > L2 between steps (outside the step's events)
+        starts[i].record(stream)
+        kstarts[i].record(stream)
+        step()
+        kends[i].record(stream)
+        gather()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kern_ms = [s.elapsed_time(e) for s, e in zip(kstarts, kends)]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    n_total = len(rays_all)
+    value = n_total * args.steps / (tot_ms / 1e3) / 1e6
+
+    result = None
+    if rank == 0:
+        # ---- end to end through the public API with host buffers (pinned)
+        hr = torch.from_numpy(np.ascontiguousarray(rays_all[own])).pin_memory()
+        hh = torch.empty((n_local, 4), dtype=torch.int32).pin_memory()
+        for _ in range(2):
+            handle.trace_host(hr, hh, restart=args.restart)
+        e2e = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            handle.trace_host(hr, hh, restart=args.restart)
+            e2e.append(time.perf_counter() - t1)
+        e2e_val = n_local / statistics.median(e2e) / 1e6 * world
+
+        # ---- roofline: algorithmic bytes per launch / measured kernel time (trace kernel)
+        kmean = statistics.mean(kern_ms)
+        alg = algorithmic_bytes(handle, rays, args.restart, n_local)
+        pk = peaks()
+        hbm = pk.get("hbm_gbs")
+        traffic = None
+        try:
+            tj = json.load(open(PROFILE_TRAFFIC))
+            key = f"{cfg}|{handle.signature}|{'restart' if args.restart else 'stack'}"
+            if key in tj:
+                traffic = tj[key]["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        achieved = alg["bytes_per_launch"] / (kmean / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 5) if hbm else None, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if hbm else "missing",
+                "algorithmic_bytes_per_ray": round(alg["bytes_per_ray"], 2), "kernel_ms": round(kmean, 4),
+                "note": "pointer-chasing; latency/issue-bound, see profiles/"}
+
+        # ---- CPU baseline (oracle) on a bounded sample + parity of the sample
+        hits_np = hits.cpu().numpy()
+        gxyz, gt = hits_np[:, :3], hits_np[:, 3].view(np.float32)
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            cpu = cpu_baseline(vol, rays_all, gxyz, gt, budget_s=args.cpu_budget)
+
+        hit_rate = float((gxyz[:, 0] >= 0).mean())
+        bpv = stats["bytes_used"] / max(nonempty, 1)
+        result = {
+            "metric": "primary-ray Mrays/s per hybrid format vs bytes/voxel",
+            "value": round(value, 2), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(tot_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg}: {desc}", "format": handle.signature, "variant":
+                       "restart" if args.restart else "stack", "volume": list(dims), "rays": n_total,
+                       "nonempty_voxels": int(nonempty), "bytes_used": stats["bytes_used"],
+                       "paper_layout_bytes": stats["paper_layout_bytes"], "bytes_per_voxel": round(bpv, 4),
+                       "bytes_per_voxel_paper": round(stats["paper_layout_bytes"] / max(nonempty, 1), 4),
+                       "hit_rate": round(hit_rate, 4), "build_s": round(build_s, 2),
+                       "l2": "flushed between timed steps (write 2x126 MB)",
+                       "parallelism": f"ray tiles 16x16 interleaved over {world} GPU(s); volume replicated"},
+            "e2e": {"value": round(e2e_val, 2), "unit": "Mrays/s", "h2d_bytes_per_step": n_local * 32,
+                    "d2h_bytes_per_step": n_local * 16},
+            "gpu_launches": args.steps,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        if args.sweep and cfg in SWEEP:
+            result["sweep"] = sweep(cfg, vol, rays, hits, stream, flush, args)
+    if world > 1:
+        dist.destroy_process_group()
+    return result
+
+
+def algorithmic_bytes(handle, rays, restart, n):
+    """Algorithmic bytes per launch: 48 B ray I/O per ray + format words read per ray as counted by
+    the counters build of the same kernel (SURVEY.md §8(d) per-step byte table)."""
+    c = handle.counters(rays, restart=restart) if hasattr(handle, "counters") else None
+    if c is None:
+        return {"bytes_per_launch": 48 * n, "bytes_per_ray": 48.0}
+    b = 48 * n + c["format_bytes"]
+    return {"bytes_per_launch": b, "bytes_per_ray": b / n, **c}
+
+
+def sweep(cfg, vol, rays, hits, stream, flush, args):
+    import torch
+    import inputs
+    from paper_2410_14128_b200 import vf
+    keys, rgba = inputs.voxels_device(vol)
+    dims = inputs.dims_of(vol)
+    out = []
+    for fmt in SWEEP[cfg]:
+        try:
+            h = vf.build((keys, rgba, dims), fmt)
+        except vf.VfError as e:
+            out.append({"format": fmt, "error": str(e)})
+            continue
+        st = h.stats()
+        for restart in (False, True):
+            for _ in range(3):
+                h.trace(rays, hits, restart=restart)
+            ms = []
+            for i in range(5):
+                flush.fill_(i)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                h.trace(rays, hits, restart=restart)
+                b.record(stream)
+                torch.cuda.synchronize()
+                ms.append(a.elapsed_time(b))
+            out.append({"format": h.signature, "variant": "restart" if restart else "stack",
+                        "mrays_s": round(rays.shape[0] / (statistics.median(ms) / 1e3) / 1e6, 1),
+                        "bytes_per_voxel": round(st["bytes_used"] / st["nonempty_voxels"], 4),
+                        "paper_bytes_per_voxel": round(st["paper_layout_bytes"] / st["nonempty_voxels"], 4),
+                        "mib": round(st["bytes_used"] / 2**20, 1)})
+        h.close()
+    return out
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores (this tier's reference arm)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    import oracle
+    cfg = args.config
+    vname, _, deffmt, desc = CONFIGS[cfg]
+    vol = make_volume(vname)
+    rays_all, _ = make_rays(cfg)
+    g = oracle.Grid.procedural(vol) if vol.gen != 5 else oracle.Grid.from_generator(vol)
+    cores = oracle.max_threads()
+    n = len(rays_all)
+    m = 4096
+    # size one step so K+W steps take about a minute in total
+    t0 = time.perf_counter()
+    g.trace(rays_all[np.linspace(0, n - 1, m).astype(np.int64)])
+    dt = time.perf_counter() - t0
+    per_ray = dt / m
+    m = int(min(n, max(1024, 60.0 / (args.steps + args.warmup) / per_ray)))
+    idx = np.linspace(0, n - 1, m).astype(np.int64)
+    sample = np.ascontiguousarray(rays_all[idx])
+    for _ in range(args.warmup):
+        g.trace(sample[: max(1, m // 8)])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        g.trace(sample)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    val = m * args.steps / tot / 1e6
+    return {"impl": "reference", "metric": "primary-ray Mrays/s per hybrid format vs bytes/voxel",
+            "value": round(val, 5), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int128-exact", "data": "synthetic",
+            "config": {"workload": f"{cfg}: {desc}", "format": "dense occupancy (oracle, no format)", "rays": n},
+            "cpu_baseline": {"value": round(val, 5), "unit": "Mrays/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{m} of {n} rays per step (evenly strided), procedural occupancy"},
+            "e2e": {"value": round(val, 5), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--format", default=None)
+    ap.add_argument("--restart", action="store_true")
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

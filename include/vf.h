@@ -161,6 +161,38 @@ VF_API vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf
 VF_API vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hit* host_hits, uint32_t trace_flags,
                         void* cuda_stream);
 
+/* ---------------------------------------------------------------- measurement aid
+ * Work counters of the counting variant of the SAME trace kernel ("Counts come
+ * from a -DVF_COUNTERS build of the same kernel"): totals over all rays of one launch.
+ * VF_CTR_FORMAT_BYTES is the algorithmic format traffic: every format word the traversal reads,
+ * counted once per read at its load width (Raw cell 4 B, SVO node 8 B, SVDAG mask 4 B + child
+ * pointer 4 B, N^3 node 16 B, leaf terminating integer 4 B); ray I/O (48 B/ray) is not included.
+ * VF_CTR_EXACT_CALLS counts exact fp64 fallbacks of the certified comparator. */
+enum {
+  VF_CTR_RAYS = 0,
+  VF_CTR_HITS,
+  VF_CTR_CELL_TESTS,    /* cells tested at any tier */
+  VF_CTR_STEPS,         /* DDA steps at any tier */
+  VF_CTR_DESCENTS,      /* child descents (ordered_hit_children -> next_intersect) */
+  VF_CTR_POPS,          /* node exits (stack pops or restarts) */
+  VF_CTR_REDESCENTS,    /* restart variant: levels re-descended from the sub-volume root */
+  VF_CTR_LOCATES,       /* certified sub-cell locates (entry + descents at stale events) */
+  VF_CTR_NEAR_TIES,     /* DDA steps whose argmin needed the pairwise exact path */
+  VF_CTR_RAW_CELLS,     /* Raw cells read (4 B) */
+  VF_CTR_SVO_NODES,     /* SVO node headers read (8 B) */
+  VF_CTR_SVDAG_NODES,   /* SVDAG masks read (4 B) */
+  VF_CTR_SVDAG_PTRS,    /* SVDAG child pointers read (4 B) */
+  VF_CTR_NTREE_NODES,   /* N^3 node headers read (16 B) */
+  VF_CTR_LEAF_WORDS,    /* leaf terminating integers read (4 B) */
+  VF_CTR_FORMAT_BYTES,  /* sum of the above in bytes */
+  VF_CTR_EXACT_CALLS,   /* exact fallbacks (device-global counter) */
+  VF_NCOUNTERS
+};
+
+/* Same as vf_trace but runs the counting variant and returns the totals (synchronous). */
+VF_API vf_status vf_trace_counters(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits,
+                                   uint32_t trace_flags, void* cuda_stream, uint64_t counters[VF_NCOUNTERS]);
+
 /* ---------------------------------------------------------------- test aids */
 /* Point query (S:400-406 analogue): rgba_out[i] = stored voxel at xyz[3i..3i+2] (device
  * uint32 triples), 0 if empty or out of range; descends the format like intersection. */

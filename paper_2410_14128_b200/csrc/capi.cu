@@ -104,6 +104,46 @@ vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* h
   return launch_trace(h, rays, n, hits, trace_flags, (cudaStream_t)cuda_stream);
 }
 
+vf_status vf_trace_counters(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t trace_flags,
+                            void* cuda_stream, uint64_t counters[VF_NCOUNTERS]) {
+  clear_error();
+  if (!h || !counters) {
+    set_error("vf_trace_counters: null argument");
+    return VF_ERR_INVALID_ARG;
+  }
+  for (int i = 0; i < VF_NCOUNTERS; ++i) counters[i] = 0;
+  if (n == 0) return VF_OK;
+  if (!rays || !hits || !aligned16(rays) || !aligned16(hits)) {
+    set_error("vf_trace_counters: rays/hits must be non-null 16-byte aligned device pointers");
+    return VF_ERR_INVALID_ARG;
+  }
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  unsigned long long* d = nullptr;
+  VF_CUDA_TRY(cudaMalloc(&d, sizeof(unsigned long long) * VF_NCOUNTERS));
+  unsigned long long ex = 0;
+  vf_status st = read_exact_calls(&ex, true);
+  if (st == VF_OK) {
+    cudaMemsetAsync(d, 0, sizeof(unsigned long long) * VF_NCOUNTERS, s);
+    st = launch_trace(h, rays, n, hits, trace_flags, s, d);
+  }
+  if (st == VF_OK) {
+    unsigned long long hc[VF_NCOUNTERS];
+    cudaError_t e = cudaMemcpyAsync(hc, d, sizeof(hc), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      set_error("vf_trace_counters: %s", cudaGetErrorString(e));
+      st = VF_ERR_CUDA;
+    } else {
+      for (int i = 0; i < VF_NCOUNTERS; ++i) counters[i] = hc[i];
+      st = read_exact_calls(&ex, true);
+      counters[VF_CTR_EXACT_CALLS] = ex;
+    }
+  }
+  cudaFree(d);
+  return st;
+}
+
 vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hit* host_hits, uint32_t trace_flags,
                         void* cuda_stream) {
   clear_error();

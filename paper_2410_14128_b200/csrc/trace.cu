@@ -55,9 +55,19 @@ struct Event {
 
 __device__ __forceinline__ float tplane(int P, float o, float inv) { return __fmul_rn(__fsub_rn((float)P, o), inv); }
 
+// Select v[i] for a run-time i without indexed (local-memory) access.
+template <class T>
+__device__ __forceinline__ T sel3(const T (&v)[3], int i) {
+  return i == 0 ? v[0] : (i == 1 ? v[1] : v[2]);
+}
+
 // ---- exact fallbacks (rare; kept out of line) -------------------------------------------
+// Number of exact fallbacks executed (statistic for the certified-filter miss rate).
+__device__ unsigned long long g_exact_calls;
+
 // sign(T_a(P) - T_b(Q)) for d_a, d_b != 0, exactly.
 __device__ __noinline__ int cmp_pp_exact(int P, float oa, float da, int Q, float ob, float db) {
+  atomicAdd(&g_exact_calls, 1ull);
   const double A = (double)P - (double)oa;  // exact (<= 52 significant bits in the domain)
   const double B = (double)Q - (double)ob;
   const double x = A * (double)db, xe = fma(A, (double)db, -x);  // TwoProduct: A*db = x + xe
@@ -68,6 +78,7 @@ __device__ __noinline__ int cmp_pp_exact(int P, float oa, float da, int Q, float
 }
 // sign(T_a(P) - s) for a scalar time s (tmin / tmax), exactly.
 __device__ __noinline__ int cmp_ps_exact(int P, float oa, float da, float s) {
+  atomicAdd(&g_exact_calls, 1ull);
   const double A = (double)P - (double)oa;
   const double S = (double)s * (double)da;  // 24 x 24 bits: exact
   int r = (A > S) - (A < S);
@@ -85,20 +96,20 @@ __device__ __forceinline__ int cert(float t1, float t2) {
 __device__ __forceinline__ int cmp_pp(const Ray& r, int a, int P, float t1, int b, int Q, float t2) {
   if (a == b) {
     const int s = (P > Q) - (P < Q);
-    return r.d[a] > 0.f ? s : -s;
+    return sel3(r.d, a) > 0.f ? s : -s;
   }
   const int c = cert(t1, t2);
   if (c != 2) return c;
-  return cmp_pp_exact(P, r.o[a], r.d[a], Q, r.o[b], r.d[b]);
+  return cmp_pp_exact(P, sel3(r.o, a), sel3(r.d, a), Q, sel3(r.o, b), sel3(r.d, b));
 }
 
 // sign(E - T_b(Q)) for an event E (plane or tmin).
 __device__ __forceinline__ int cmp_ep(const Ray& r, const Event& E, int b, int Q) {
-  const float tq = tplane(Q, r.o[b], r.inv[b]);
+  const float tq = tplane(Q, sel3(r.o, b), sel3(r.inv, b));
   if (E.axis == TMIN_AXIS) {
     const int c = cert(E.t, tq);
     if (c != 2) return c;
-    return -cmp_ps_exact(Q, r.o[b], r.d[b], E.t);
+    return -cmp_ps_exact(Q, sel3(r.o, b), sel3(r.d, b), E.t);
   }
   return cmp_pp(r, E.axis, E.P, E.t, b, Q, tq);
 }
@@ -109,7 +120,7 @@ __device__ __forceinline__ int cmp_ee(const Ray& r, const Event& E1, const Event
     if (E1.axis == TMIN_AXIS) return 0;
     const int c = cert(E1.t, E2.t);
     if (c != 2) return c;
-    return cmp_ps_exact(E1.P, r.o[E1.axis], r.d[E1.axis], E2.t);
+    return cmp_ps_exact(E1.P, sel3(r.o, E1.axis), sel3(r.d, E1.axis), E2.t);
   }
   return cmp_ep(r, E1, E2.axis, E2.P);
 }
@@ -119,14 +130,14 @@ __device__ __forceinline__ int cmp_es(const Ray& r, const Event& E, float s) {
   if (E.axis == TMIN_AXIS) return (E.t > s) - (E.t < s);
   const int c = cert(E.t, s);
   if (c != 2) return c;
-  return cmp_ps_exact(E.P, r.o[E.axis], r.d[E.axis], s);
+  return cmp_ps_exact(E.P, sel3(r.o, E.axis), sel3(r.d, E.axis), s);
 }
 
 // Finest cell index on axis b at event E (right limit), known to lie in [lo, hi]:
 //   d_b > 0: T_b(k) <= E < T_b(k+1);   d_b < 0: T_b(k+1) <= E < T_b(k).
 // Candidate from fp32, then certified corrections (planes lo / hi+1 are known crossed /
 // not crossed and are never compared).
-__device__ __noinline__ int locate(const Ray& r, const Event& E, int b, int lo, int hi) {
+__device__ __forceinline__ int locate(const Ray& r, const Event& E, int b, int lo, int hi) {
   const float x = fmaf(E.t, r.d[b], r.o[b]);
   float kf = r.d[b] > 0.f ? floorf(x) : ceilf(x) - 1.0f;
   kf = fminf(fmaxf(kf, (float)lo), (float)hi);
@@ -159,13 +170,17 @@ __device__ __noinline__ int locate(const Ray& r, const Event& E, int b, int lo, 
   return k;
 }
 
-// Exact argmin of the three next-plane events (ties step together). c = candidate mask.
-__device__ __noinline__ int argmin_exact(const Ray& r, const int P[3], const float t[3], int c) {
+// Exact argmin of the three next-plane events (ties step together). c = candidate mask (>= 2
+// bits). Returns the set of minimal axes | (one minimal axis << 4).
+__device__ __forceinline__ int argmin_exact(const Ray& r, int P0, int P1, int P2, float t0, float t1, float t2, int c) {
+  const int P[3] = {P0, P1, P2};
+  const float t[3] = {t0, t1, t2};
   int best = __ffs(c) - 1;
   int set = 1 << best;
-  for (int a = best + 1; a < 3; ++a) {
-    if (!((c >> a) & 1)) continue;
-    const int s = cmp_pp(r, a, P[a], t[a], best, P[best], t[best]);
+#pragma unroll
+  for (int a = 1; a < 3; ++a) {
+    if (a <= best || !((c >> a) & 1)) continue;
+    const int s = cmp_pp(r, a, P[a], t[a], best, sel3(P, best), sel3(t, best));
     if (s < 0) {
       best = a;
       set = 1 << a;
@@ -189,8 +204,33 @@ struct Header {
   uint32_t base;  // SVO: first child; SVDAG: node address; N^3: children block
 };
 
-template <uint32_t KINDS>
-__device__ __forceinline__ Header load_header(const uint32_t* __restrict__ buf, uint32_t kind, uint32_t N) {
+// Per-ray work counters of the VF_COUNTERS variant (SURVEY.md §8(d) "Counts come from a
+// -DVF_COUNTERS build of the same kernel"). Compiled away when COUNT == false.
+template <bool COUNT>
+struct Ctr {
+  uint32_t v[VF_NCOUNTERS];
+  __device__ __forceinline__ Ctr() {
+    if (COUNT)
+#pragma unroll
+      for (int i = 0; i < VF_NCOUNTERS; ++i) v[i] = 0;
+  }
+  __device__ __forceinline__ void add(int i, uint32_t x = 1) {
+    if (COUNT) v[i] += x;
+  }
+  __device__ __forceinline__ void flush(unsigned long long* out) {
+    if (!COUNT) return;
+#pragma unroll
+    for (int i = 0; i < VF_NCOUNTERS; ++i) {
+      unsigned long long x = v[i];
+      for (int o = 16; o; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, x);
+    }
+  }
+};
+
+template <uint32_t KINDS, bool COUNT>
+__device__ __forceinline__ Header load_header(const uint32_t* __restrict__ buf, uint32_t kind, uint32_t N,
+                                              Ctr<COUNT>& ct) {
   Header h;
   h.mask = 0;
   h.base = N;
@@ -198,22 +238,29 @@ __device__ __forceinline__ Header load_header(const uint32_t* __restrict__ buf, 
     const uint2 v = __ldg(reinterpret_cast<const uint2*>(buf + N));
     h.base = v.x;
     h.mask = v.y & 0xFFu;
+    ct.add(VF_CTR_SVO_NODES);
+    ct.add(VF_CTR_FORMAT_BYTES, 8);
   } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
     h.mask = __ldg(buf + N) & 0xFFu;
+    ct.add(VF_CTR_SVDAG_NODES);
+    ct.add(VF_CTR_FORMAT_BYTES, 4);
   } else if (has_kind<KINDS>(K_NTREE) && kind == K_NTREE) {
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(buf + N));
     h.mask = (uint64_t)v.x | ((uint64_t)v.y << 32);
     h.base = v.z;
+    ct.add(VF_CTR_NTREE_NODES);
+    ct.add(VF_CTR_FORMAT_BYTES, 16);
   }
   return h;
 }
 
-template <uint32_t KINDS, bool RESTART>
+template <uint32_t KINDS, bool RESTART, bool COUNT>
 __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
-                                                    uint64_t n) {
+                                                    uint64_t n, unsigned long long* __restrict__ counters) {
   const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (gid >= n) return;
+  Ctr<COUNT> ct;
+  if (gid < n) {
   const float4 r0 = __ldg(rays + 2 * gid), r1 = __ldg(rays + 2 * gid + 1);
   int4 out = make_int4(-1, -1, -1, __float_as_int(__int_as_float(0x7f800000)));
   Ray r;
@@ -232,6 +279,7 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
     // ---- root function: word 0, root-box test ---------------------------
     if (p.root == 0) break;  // empty volume: buffer [0]
     int moving = 0;
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (r.d[a] != 0.f) moving |= 1 << a;
       r.inv[a] = r.d[a] != 0.f ? __frcp_rn(r.d[a]) : 0.f;
@@ -240,6 +288,7 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
     if (!(r.tmin < r.tmax) && tmax_finite) break;
     Event E{TMIN_AXIS, 0, r.tmin};
     bool miss = false;
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (!((moving >> a) & 1)) {
         // half-open membership: floor(o_a) in [0, R_a)
@@ -251,7 +300,8 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
       if (cmp_ee(r, Ea, E) > 0) E = Ea;
     }
     if (miss) break;
-    for (int a = 0; a < 3 && !miss; ++a) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
       if (!((moving >> a) & 1)) continue;
       const int Px = r.d[a] > 0.f ? R[a] : 0;
       if (cmp_ep(r, E, a, Px) >= 0) miss = true;  // entered at / after the exit of slab a
@@ -260,7 +310,9 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
 
     // ---- entry cell (exact right limit at t_start) -------------------------------------
     int V[3];
+#pragma unroll
     for (int b = 0; b < 3; ++b) V[b] = ((moving >> b) & 1) ? locate(r, E, b, 0, R[b] - 1) : (int)floorf(r.o[b]);
+    ct.add(VF_CTR_LOCATES, 3);
 
     // ---- flattened per-level traversal ---------------------------------------------------
     const int T = (int)p.n_tiers;
@@ -268,7 +320,7 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
     uint32_t N = p.root;
     uint32_t stk[VF_MAX_TIERS];
     uint32_t kind = p.kind_pack & 3u;
-    Header hd = load_header<KINDS>(buf, kind, N);
+    Header hd = load_header<KINDS>(buf, kind, N, ct);
     int stale = 0;
     bool hit = false;
     // Invariant at the top of the loop: V >> lc(t) is the current (untested) cell of node N
@@ -286,11 +338,14 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
         const bool finest = t == T - 1;
         bool occ = false;
         uint32_t child = 0;
+        ct.add(VF_CTR_CELL_TESTS);
         if (has_kind<KINDS>(K_RAW) && kind == K_RAW) {
           // 64-bit index: a single-level R(11^3) grid has 2^33 cells (reading A15)
           const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
           child = __ldg(buf + (size_t)N + lin);
           occ = child != 0u;
+          ct.add(VF_CTR_RAW_CELLS);
+          ct.add(VF_CTR_FORMAT_BYTES, 4);
         } else {
           const uint32_t lin = lx + (ly << sx) + (lz << sxy);
           occ = (hd.mask >> lin) & 1u;
@@ -300,10 +355,16 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
               child = hd.base + 2u * rank;
             } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
               child = __ldg(buf + hd.base + 1u + rank);
+              ct.add(VF_CTR_SVDAG_PTRS);
+              ct.add(VF_CTR_FORMAT_BYTES, 4);
             } else {
               child = hd.base + (last ? 1u : 4u) * rank;
             }
-            if (last) child = __ldg(buf + child);  // leaf TermInt -> next level's root
+            if (last) {  // leaf TermInt -> next level's root
+              child = __ldg(buf + child);
+              ct.add(VF_CTR_LEAF_WORDS);
+              ct.add(VF_CTR_FORMAT_BYTES, 4);
+            }
           }
         }
         if (occ) {
@@ -313,22 +374,26 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
           }
           // descend at event E: make the sub-cell bits of stale axes exact
           if (stale) {
+#pragma unroll
             for (int b = 0; b < 3; ++b)
               if ((stale >> b) & 1) {
                 const int lo = (V[b] >> lc) << lc;
                 V[b] = locate(r, E, b, lo, lo + (1 << lc) - 1);
+                ct.add(VF_CTR_LOCATES);
               }
             stale = 0;
           }
-          if (!RESTART || ((p.top_mask >> t) & 1u) || kind == K_RAW) stk[t] = N;
+          if (!RESTART || ((p.top_mask >> t) & 1u)) stk[t] = N;
           ++t;
           N = child;
           kind = (p.kind_pack >> (2 * t)) & 3u;
-          hd = load_header<KINDS>(buf, kind, N);
+          hd = load_header<KINDS>(buf, kind, N, ct);
+          ct.add(VF_CTR_DESCENTS);
           continue;
         }
       }
       // -- step: exact next event among the three axes at this tier's cell size
+      ct.add(VF_CTR_STEPS);
       int Pn[3];
       float tn[3];
 #pragma unroll
@@ -345,13 +410,14 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
         S = c;
         a0 = __ffs(c) - 1;
       } else {
-        const int res = argmin_exact(r, Pn, tn, c);
+        const int res = argmin_exact(r, Pn[0], Pn[1], Pn[2], tn[0], tn[1], tn[2], c);
         S = res & 7;
         a0 = res >> 4;
+        ct.add(VF_CTR_NEAR_TIES);
       }
       E.axis = a0;
-      E.P = Pn[a0];
-      E.t = tn[a0];
+      E.P = sel3(Pn, a0);
+      E.t = sel3(tn, a0);
       if (tmax_finite && cmp_es(r, E, r.tmax) >= 0) break;  // segment ends (reading A7)
       uint32_t h = 0;
       bool out_of_box = false;
@@ -368,42 +434,54 @@ __global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const u
       stale &= ~S;
       const int tau = (int)field4(p.tau_pack, h);
       if (tau < t) {
+        ct.add(VF_CTR_POPS);
         // left the current node: pop (stack) or restart from the level root
         if (!RESTART) {
           t = tau;
           N = stk[t];
           kind = (p.kind_pack >> (2 * t)) & 3u;
-          hd = load_header<KINDS>(buf, kind, N);
+          hd = load_header<KINDS>(buf, kind, N, ct);
         } else {
           const int top = (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tau);
           t = top;
           N = stk[t];
           kind = (p.kind_pack >> (2 * t)) & 3u;
-          hd = load_header<KINDS>(buf, kind, N);
+          hd = load_header<KINDS>(buf, kind, N, ct);
           while (t < tau) {  // re-descend through nodes that contain the current cell
             const uint32_t lct = field4(p.lc_pack, t), lf = field4(p.lf_pack, t);
             const uint32_t msk = t == 0 ? 0xFFFFFFFFu : ((1u << lf) - 1u);
-            const uint32_t lin = (((uint32_t)V[0] >> lct) & msk) + ((((uint32_t)V[1] >> lct) & msk) << (t == 0 ? p.lf0[0] : lf)) +
+            const uint32_t lin = (((uint32_t)V[0] >> lct) & msk) +
+                                 ((((uint32_t)V[1] >> lct) & msk) << (t == 0 ? p.lf0[0] : lf)) +
                                  ((((uint32_t)V[2] >> lct) & msk) << (t == 0 ? p.lf0[0] + p.lf0[1] : 2 * lf));
             const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
             uint32_t child;
-            if (has_kind<KINDS>(K_SVO) && kind == K_SVO)
+            if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
               child = hd.base + 2u * rank;
-            else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG)
+            } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
               child = __ldg(buf + hd.base + 1u + rank);
-            else
+              ct.add(VF_CTR_SVDAG_PTRS);
+              ct.add(VF_CTR_FORMAT_BYTES, 4);
+            } else {
               child = hd.base + 4u * rank;  // N^3 internal (t < tau <= last tier of the level)
+            }
             ++t;
             N = child;
             kind = (p.kind_pack >> (2 * t)) & 3u;
-            hd = load_header<KINDS>(buf, kind, N);
+            hd = load_header<KINDS>(buf, kind, N, ct);
+            ct.add(VF_CTR_REDESCENTS);
           }
         }
       }
     }
-    if (hit) out = make_int4(V[0], V[1], V[2], __float_as_int(E.t));
+    if (hit) {
+      out = make_int4(V[0], V[1], V[2], __float_as_int(E.t));
+      ct.add(VF_CTR_HITS);
+    }
   } while (0);
   hits[gid] = out;
+  ct.add(VF_CTR_RAYS);
+  }
+  ct.flush(counters);
 }
 
 // ---- point query: integer-only descent (test aid) ------------------------------------------
@@ -463,17 +541,20 @@ __global__ void query_kernel(const TraceParams p, const uint32_t* __restrict__ b
   }
 }
 
-using KernelFn = void (*)(const TraceParams, const uint32_t*, const float4*, int4*, uint64_t);
+using KernelFn = void (*)(const TraceParams, const uint32_t*, const float4*, int4*, uint64_t, unsigned long long*);
 
 template <uint32_t K>
 struct Table {
-  static KernelFn get(bool restart) { return restart ? trace_kernel<K, true> : trace_kernel<K, false>; }
+  static KernelFn get(bool restart, bool count) {
+    if (count) return restart ? trace_kernel<K, true, true> : trace_kernel<K, false, true>;
+    return restart ? trace_kernel<K, true, false> : trace_kernel<K, false, false>;
+  }
 };
 
-KernelFn select_kernel(uint32_t kinds, bool restart) {
+KernelFn select_kernel(uint32_t kinds, bool restart, bool count) {
   switch (kinds) {
 #define VF_CASE(k) \
-  case k: return Table<k>::get(restart);
+  case k: return Table<k>::get(restart, count);
     VF_CASE(1) VF_CASE(2) VF_CASE(3) VF_CASE(4) VF_CASE(5) VF_CASE(6) VF_CASE(7) VF_CASE(8) VF_CASE(9) VF_CASE(10)
     VF_CASE(11) VF_CASE(12) VF_CASE(13) VF_CASE(14) VF_CASE(15)
 #undef VF_CASE
@@ -483,11 +564,12 @@ KernelFn select_kernel(uint32_t kinds, bool restart) {
 
 }  // namespace
 
-vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags, cudaStream_t s) {
+vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags, cudaStream_t s,
+                       unsigned long long* counters) {
   if (n == 0) return VF_OK;
   uint32_t kinds = 0;
   for (uint32_t t = 0; t < h->fmt.n_tiers; ++t) kinds |= 1u << h->fmt.tiers[t].kind;
-  KernelFn fn = select_kernel(kinds, (flags & VF_TRACE_RESTART_SV) != 0);
+  KernelFn fn = select_kernel(kinds, (flags & VF_TRACE_RESTART_SV) != 0, counters != nullptr);
   if (!fn) {
     set_error("vf_trace: no kernel instantiated for kind set 0x%x", kinds);
     return VF_ERR_UNSUPPORTED;
@@ -499,11 +581,20 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     return VF_ERR_INVALID_ARG;
   }
   fn<<<(unsigned)blocks, threads, 0, s>>>(h->tp, h->buf, reinterpret_cast<const float4*>(rays),
-                                          reinterpret_cast<int4*>(hits), n);
+                                          reinterpret_cast<int4*>(hits), n, counters);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("vf_trace: launch failed: %s", cudaGetErrorString(e));
     return VF_ERR_CUDA;
+  }
+  return VF_OK;
+}
+
+vf_status read_exact_calls(unsigned long long* out, bool reset) {
+  VF_CUDA_TRY(cudaMemcpyFromSymbol(out, g_exact_calls, sizeof(*out)));
+  if (reset) {
+    const unsigned long long z = 0;
+    VF_CUDA_TRY(cudaMemcpyToSymbol(g_exact_calls, &z, sizeof(z)));
   }
   return VF_OK;
 }

@@ -84,7 +84,8 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
 
 // trace.cu
 vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags,
-                       cudaStream_t s);
+                       cudaStream_t s, unsigned long long* counters = nullptr);
+vf_status read_exact_calls(unsigned long long* out, bool reset);
 vf_status launch_query(const Handle* h, const uint32_t* xyz, uint64_t n, uint32_t* out, cudaStream_t s);
 
 #define VF_CUDA_TRY(expr)                                                                   \

@@ -29,6 +29,10 @@ VF_BUILD_DEFAULT = VF_BUILD_WHOLE_LEVEL_DEDUP
 VF_TRACE_RESTART_SV = 1
 VF_MAX_LEVELS = 16
 VF_MAX_TIERS = 16
+COUNTER_NAMES = ("rays", "hits", "cell_tests", "steps", "descents", "pops", "redescents", "locates", "near_ties",
+                 "raw_cells", "svo_nodes", "svdag_nodes", "svdag_ptrs", "ntree_nodes", "leaf_words", "format_bytes",
+                 "exact_calls")
+VF_NCOUNTERS = len(COUNTER_NAMES)
 
 
 class VfError(RuntimeError):
@@ -67,6 +71,7 @@ _sig = {
                   ctypes.POINTER(_u64)], ctypes.c_int),
     "vf_trace": ([_vp, _vp, _u64, _vp, _u32, _vp], ctypes.c_int),
     "vf_trace_host": ([_vp, _vp, _u64, _vp, _u32, _vp], ctypes.c_int),
+    "vf_trace_counters": ([_vp, _vp, _u64, _vp, _u32, _vp, ctypes.POINTER(_u64)], ctypes.c_int),
     "vf_query": ([_vp, _vp, _u64, _vp, _vp], ctypes.c_int),
     "vf_stats_get": ([_vp, ctypes.POINTER(Stats)], ctypes.c_int),
     "vf_buffer": ([_vp, ctypes.POINTER(_vp), ctypes.POINTER(_u64)], ctypes.c_int),
@@ -195,6 +200,17 @@ class Handle:
         _check(_lib.vf_trace(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
                              VF_TRACE_RESTART_SV if restart else 0, _stream_ptr(stream)))
         return hits
+
+    def counters(self, rays, hits=None, restart: bool = False, stream=None) -> dict:
+        """Run the counting variant of the trace kernel once; totals over all rays (synchronous)."""
+        import torch
+        n = rays.shape[0]
+        if hits is None:
+            hits = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        c = (_u64 * VF_NCOUNTERS)()
+        _check(_lib.vf_trace_counters(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
+                                      VF_TRACE_RESTART_SV if restart else 0, _stream_ptr(stream), c))
+        return {k: int(c[i]) for i, k in enumerate(COUNTER_NAMES)}
 
     def trace_host(self, rays, hits, restart: bool = False, stream=None):
         """End to end: host (pinned) rays (n,8) float32 -> host hits (n,4) int32, copies inside."""
