@@ -68,13 +68,6 @@ def make_rays(cfg):
     return R.camera(cam)
 
 
-def shard_tiles(width, height, perm, rank, world, tile=16):
-    """Indices (into the tile-ordered ray array) owned by `rank`: 16x16 screen tiles, tile mod N."""
-    px, py = perm % width, perm // width
-    tid = (py // tile) * ((width + tile - 1) // tile) + (px // tile)
-    return np.nonzero(tid % world == rank)[0]
-
-
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
 
@@ -158,10 +151,6 @@ def cpu_baseline(vol_desc, rays, gpu_xyz, gpu_t, budget_s=12.0):
             "parity_checked": checked, "parity_mismatches": bad}
 
 
-def counters_for(handle, rays_dev, restart):
-    return None
-
-
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -190,32 +179,25 @@ def run_ours(args):
     stats = handle.stats()
 
     rays_all, perm = make_rays(cfg)
-    W = int(perm.max() + 1)
-    width = {"cfg1": 256}.get(cfg, None)
     from inputs.rays import CAMERAS
+    from paper_2410_14128_b200 import shard
     cam = CONFIGS[cfg][1]
-    width, height = (256, 256) if cam is None else (CAMERAS[cam]["width"], CAMERAS[cam]["height"])
-    own = shard_tiles(width, height, perm, rank, world) if world > 1 else np.arange(len(rays_all))
+    width = 256 if cam is None else CAMERAS[cam]["width"]
+    own = shard.shard(perm, width, rank, world)
     rays = torch.from_numpy(np.ascontiguousarray(rays_all[own])).to(dev)
     n_local = rays.shape[0]
     hits = torch.empty((n_local, 4), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
 
-    # gather buffers (rank 0)
-    counts = [len(shard_tiles(width, height, perm, r, world)) for r in range(world)] if world > 1 else [n_local]
+    counts = shard.shard_counts(perm, width, world)
 
     def step():
         handle.trace(rays, hits, restart=args.restart)
 
-    def gather():
-        if world == 1:
-            return
-        if rank == 0:
-            bufs = [torch.empty((c, 4), dtype=torch.int32, device=dev) for c in counts]
-            dist.gather(hits, gather_list=bufs, dst=0)
-        else:
-            dist.gather(hits, dst=0)
+    def gather():  # the one collective: hit buffers to rank 0 (NCCL)
+        if world > 1:
+            shard.gather_hits(hits, counts)
 
     for _ in range(args.warmup):
         step()

@@ -146,6 +146,7 @@ enum {
                                    stackless — after leaving a node of an SVO / SVDAG / N^3-tree
                                    level, re-descend from that level's sub-volume root instead
                                    of popping a per-thread stack. Results are identical. */
+  /* bit 30 is reserved (internal ablation: persistent warps with dynamic ray refill) */
 };
 
 /* Trace n rays (device array) into hits (device array), one thread per ray, asynchronously

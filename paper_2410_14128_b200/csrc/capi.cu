@@ -80,6 +80,17 @@ vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_leve
     return st;
   }
   h->tp = make_trace_params(f, h->stats.root);
+  {
+    cudaError_t e = cudaMalloc(&h->work, sizeof(unsigned long long) * 2 * kWorkSlots);
+    if (e == cudaSuccess) e = cudaMemset(h->work, 0, sizeof(unsigned long long) * 2 * kWorkSlots);
+    if (e != cudaSuccess) {
+      set_error("vf_build: work-counter allocation failed: %s", cudaGetErrorString(e));
+      if (h->work) cudaFree(h->work);
+      cudaFree(h->buf);
+      delete h;
+      return VF_ERR_OOM;
+    }
+  }
   for (int a = 0; a < 3; ++a) h->stats.dims[a] = f.dims[a];
   h->stats.n_levels = f.n_levels;
   h->stats.n_tiers = f.n_tiers;
@@ -239,6 +250,7 @@ void vf_destroy(vf_handle* h) {
   DeviceGuard g(h->device);
   if (h->buf) cudaFree(h->buf);
   if (h->stage) cudaFree(h->stage);
+  if (h->work) cudaFree(h->work);
   delete h;
 }
 

@@ -299,6 +299,7 @@ TraceParams make_trace_params(const Format& f, uint32_t root) {
   }
   p.n_tiers = f.n_tiers;
   p.root = root;
+  p.refill = 12;
   return p;
 }
 
@@ -351,7 +352,6 @@ vf_status vf_format_resolution(const vf_level* levels, uint32_t n, uint32_t dims
   clear_error();
   Format f;
   // DF levels have a resolution even though this build cannot construct them
-  bool has_df = false;
   vf_level tmp[VF_MAX_LEVELS];
   if (n > VF_MAX_LEVELS || !levels || !dims) {
     set_error("vf_format_resolution: bad arguments");
@@ -359,14 +359,10 @@ vf_status vf_format_resolution(const vf_level* levels, uint32_t n, uint32_t dims
   }
   for (uint32_t l = 0; l < n; ++l) {
     tmp[l] = levels[l];
-    if (tmp[l].kind == VF_DF) {
-      has_df = true;
-      tmp[l].kind = VF_RAW;
-    }
+    if (tmp[l].kind == VF_DF) tmp[l].kind = VF_RAW;
   }
   vf_status st = expand_format(tmp, n, &f);
   if (st != VF_OK) return st;
-  (void)has_df;
   for (int a = 0; a < 3; ++a) dims[a] = f.dims[a];
   return VF_OK;
 }

@@ -34,6 +34,10 @@
 // returns the same voxel, bit for bit.
 #include <stdint.h>
 
+#include <stdlib.h>
+
+#include <mutex>
+
 #include "vf_internal.cuh"
 
 namespace vf {
@@ -66,7 +70,7 @@ __device__ __forceinline__ T sel3(const T (&v)[3], int i) {
 __device__ unsigned long long g_exact_calls;
 
 // sign(T_a(P) - T_b(Q)) for d_a, d_b != 0, exactly.
-__device__ __noinline__ int cmp_pp_exact(int P, float oa, float da, int Q, float ob, float db) {
+__device__ __forceinline__ int cmp_pp_exact(int P, float oa, float da, int Q, float ob, float db) {
   atomicAdd(&g_exact_calls, 1ull);
   const double A = (double)P - (double)oa;  // exact (<= 52 significant bits in the domain)
   const double B = (double)Q - (double)ob;
@@ -77,7 +81,7 @@ __device__ __noinline__ int cmp_pp_exact(int P, float oa, float da, int Q, float
   return ((da > 0.f) == (db > 0.f)) ? s : -s;  // T1 - T2 = (A db - B da) / (da db)
 }
 // sign(T_a(P) - s) for a scalar time s (tmin / tmax), exactly.
-__device__ __noinline__ int cmp_ps_exact(int P, float oa, float da, float s) {
+__device__ __forceinline__ int cmp_ps_exact(int P, float oa, float da, float s) {
   atomicAdd(&g_exact_calls, 1ull);
   const double A = (double)P - (double)oa;
   const double S = (double)s * (double)da;  // 24 x 24 bits: exact
@@ -133,22 +137,38 @@ __device__ __forceinline__ int cmp_es(const Ray& r, const Event& E, float s) {
   return cmp_ps_exact(E.P, sel3(r.o, E.axis), sel3(r.d, E.axis), s);
 }
 
+// sign(E - T_b(Q)) with every operand passed as a scalar (for the out-of-line slow paths, so the
+// ray never has to be spilled to local memory for a call).
+__device__ __forceinline__ int cmp_ep_s(int eaxis, int eP, float et, float oa, float da, int b, int Q, float ob,
+                                        float db, float invb) {
+  if (eaxis == b) {
+    const int s = (eP > Q) - (eP < Q);
+    return db > 0.f ? s : -s;
+  }
+  const float tq = tplane(Q, ob, invb);
+  const int c = cert(et, tq);
+  if (c != 2) return c;
+  if (eaxis == TMIN_AXIS) return -cmp_ps_exact(Q, ob, db, et);
+  return cmp_pp_exact(eP, oa, da, Q, ob, db);
+}
+
 // Finest cell index on axis b at event E (right limit), known to lie in [lo, hi]:
 //   d_b > 0: T_b(k) <= E < T_b(k+1);   d_b < 0: T_b(k+1) <= E < T_b(k).
-// Candidate from fp32, then certified corrections (planes lo / hi+1 are known crossed /
-// not crossed and are never compared).
-__device__ __forceinline__ int locate(const Ray& r, const Event& E, int b, int lo, int hi) {
-  const float x = fmaf(E.t, r.d[b], r.o[b]);
-  float kf = r.d[b] > 0.f ? floorf(x) : ceilf(x) - 1.0f;
+// Slow path: candidate from fp32, then certified plane comparisons (planes lo / hi+1 are known
+// crossed / not crossed and are never compared). oa / da: origin / direction on E's axis.
+__device__ __forceinline__ int locate_slow(int b, float ob, float db, float invb, int eaxis, int eP, float et, float oa,
+                                        float da, int lo, int hi) {
+  const float x = fmaf(et, db, ob);
+  float kf = db > 0.f ? floorf(x) : ceilf(x) - 1.0f;
   kf = fminf(fmaxf(kf, (float)lo), (float)hi);
   int k = (int)kf;
-  if (r.d[b] > 0.f) {
+  if (db > 0.f) {
     for (;;) {
-      if (k > lo && cmp_ep(r, E, b, k) < 0) {
+      if (k > lo && cmp_ep_s(eaxis, eP, et, oa, da, b, k, ob, db, invb) < 0) {
         --k;
         continue;
       }
-      if (k < hi && cmp_ep(r, E, b, k + 1) >= 0) {
+      if (k < hi && cmp_ep_s(eaxis, eP, et, oa, da, b, k + 1, ob, db, invb) >= 0) {
         ++k;
         continue;
       }
@@ -156,11 +176,11 @@ __device__ __forceinline__ int locate(const Ray& r, const Event& E, int b, int l
     }
   } else {
     for (;;) {
-      if (k < hi && cmp_ep(r, E, b, k + 1) < 0) {
+      if (k < hi && cmp_ep_s(eaxis, eP, et, oa, da, b, k + 1, ob, db, invb) < 0) {
         ++k;
         continue;
       }
-      if (k > lo && cmp_ep(r, E, b, k) >= 0) {
+      if (k > lo && cmp_ep_s(eaxis, eP, et, oa, da, b, k, ob, db, invb) >= 0) {
         --k;
         continue;
       }
@@ -170,17 +190,41 @@ __device__ __forceinline__ int locate(const Ray& r, const Event& E, int b, int l
   return k;
 }
 
+// Fast path: the position x = o_b + T_E d_b is computed as x^ = fma(T^_E, d_b, o_b) with
+// |x^ - x| <= 3.01u|T d_b| + 1.01u|x^| (T^_E has relative error <= 3u, one rounding in the fma),
+// so B = 2^-21 (|T^ d_b| + |x^|) >= 8u(...) bounds it with margin. If [x^-B, x^+B] contains no
+// integer, x is not on a plane and tau_b(E+) = floor(x) = floor(x^) for either sign of d_b.
+// Otherwise (ray on / near a plane at E: ~0.2% of calls) the certified slow path decides.
+__device__ __forceinline__ int locate(const Ray& r, const Event& E, int b, int lo, int hi) {
+  const float db = sel3(r.d, b), ob = sel3(r.o, b);
+  const float x = fmaf(E.t, db, ob);
+  const float fl = floorf(x);
+  const float f = x - fl;  // exact
+  const float B = (fabsf(E.t * db) + fabsf(x)) * 0x1p-21f;
+  const int k = (int)fl;
+  if (f > B && 1.0f - f > B && k >= lo && k <= hi) return k;
+  const int ea = E.axis > 2 ? 0 : E.axis;
+  return locate_slow(b, ob, db, sel3(r.inv, b), E.axis, E.P, E.t, sel3(r.o, ea), sel3(r.d, ea), lo, hi);
+}
+
 // Exact argmin of the three next-plane events (ties step together). c = candidate mask (>= 2
 // bits). Returns the set of minimal axes | (one minimal axis << 4).
-__device__ __forceinline__ int argmin_exact(const Ray& r, int P0, int P1, int P2, float t0, float t1, float t2, int c) {
+__device__ __forceinline__ int argmin_exact(float o0, float o1, float o2, float d0, float d1, float d2, int P0, int P1,
+                                         int P2, float t0, float t1, float t2, int c) {
+  const float o[3] = {o0, o1, o2}, d[3] = {d0, d1, d2}, t[3] = {t0, t1, t2};
   const int P[3] = {P0, P1, P2};
-  const float t[3] = {t0, t1, t2};
   int best = __ffs(c) - 1;
   int set = 1 << best;
 #pragma unroll
   for (int a = 1; a < 3; ++a) {
     if (a <= best || !((c >> a) & 1)) continue;
-    const int s = cmp_pp(r, a, P[a], t[a], best, sel3(P, best), sel3(t, best));
+    // a != best: different axes
+    int s;
+    const int cc = cert(t[a], sel3(t, best));
+    if (cc != 2)
+      s = cc;
+    else
+      s = cmp_pp_exact(P[a], o[a], d[a], sel3(P, best), sel3(o, best), sel3(d, best));
     if (s < 0) {
       best = a;
       set = 1 << a;
@@ -218,12 +262,13 @@ struct Ctr {
     if (COUNT) v[i] += x;
   }
   __device__ __forceinline__ void flush(unsigned long long* out) {
-    if (!COUNT) return;
+    if constexpr (COUNT) {
 #pragma unroll
-    for (int i = 0; i < VF_NCOUNTERS; ++i) {
-      unsigned long long x = v[i];
-      for (int o = 16; o; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-      if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, x);
+      for (int i = 0; i < VF_NCOUNTERS; ++i) {
+        unsigned long long x = v[i];
+        for (int o = 16; o; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, x);
+      }
     }
   }
 };
@@ -254,234 +299,344 @@ __device__ __forceinline__ Header load_header(const uint32_t* __restrict__ buf, 
   return h;
 }
 
-template <uint32_t KINDS, bool RESTART, bool COUNT>
-__global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
-                                                    const float4* __restrict__ rays, int4* __restrict__ hits,
-                                                    uint64_t n, unsigned long long* __restrict__ counters) {
-  const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  Ctr<COUNT> ct;
-  if (gid < n) {
-  const float4 r0 = __ldg(rays + 2 * gid), r1 = __ldg(rays + 2 * gid + 1);
-  int4 out = make_int4(-1, -1, -1, __float_as_int(__int_as_float(0x7f800000)));
-  Ray r;
-  r.o[0] = r0.x;
-  r.o[1] = r0.y;
-  r.o[2] = r0.z;
-  r.tmin = r0.w;
-  r.d[0] = r1.x;
-  r.d[1] = r1.y;
-  r.d[2] = r1.z;
-  r.tmax = r1.w;
-  const bool tmax_finite = r.tmax < __int_as_float(0x7f800000);
-  const int R[3] = {p.dims[0], p.dims[1], p.dims[2]};
+enum { IT_CONTINUE = 0, IT_HIT = 1, IT_MISS = 2 };
 
-  do {
-    // ---- root function: word 0, root-box test ---------------------------
-    if (p.root == 0) break;  // empty volume: buffer [0]
-    int moving = 0;
+// The per-ray traversal state machine: start() is the root function, iterate() is one cell test
+// followed by either a descent or one DDA step (with pop / restart when the step leaves a node).
+// Per-tier parameters of the current tier are cached in registers and refreshed only when the
+// tier changes (descent, pop, restart).
+template <uint32_t KINDS, bool RESTART, bool COUNT>
+struct Lane {
+  Ray r;
+  Event E;
+  int V[3];       // finest voxel of the current cell (bits below lc(t) valid unless stale)
+  int t;          // current tier
+  uint32_t N;     // current node (word address)
+  uint32_t kind;  // kind of tier t
+  Header hd;
+  int stale;   // axes whose sub-cell bits are not exact at E
+  int moving;  // axes with d != 0
+  int dneg;    // axes with d < 0
+  bool tmax_finite;
+  // cached parameters of tier t
+  uint32_t lc, msk, sx, sxy;
+  bool last, finest;
+  // (the per-tier node stack lives outside the struct so that the struct itself can stay in
+  //  registers: an indexed member would force the whole object into local memory)
+
+  __device__ __forceinline__ void set_tier(const TraceParams& p, int nt) {
+    t = nt;
+    kind = (p.kind_pack >> (2 * nt)) & 3u;
+    lc = field4(p.lc_pack, nt);
+    const uint32_t lf = field4(p.lf_pack, nt);
+    msk = nt == 0 ? 0xFFFFFFFFu : ((1u << lf) - 1u);
+    sx = nt == 0 ? p.lf0[0] : lf;
+    sxy = nt == 0 ? p.lf0[0] + p.lf0[1] : 2 * lf;
+    last = (p.last_mask >> nt) & 1u;
+    finest = nt == (int)p.n_tiers - 1;
+  }
+
+  // ---- root function: word 0, root-box test, exact entry cell ---------------
+  __device__ __forceinline__ bool start(const TraceParams& p, const uint32_t* __restrict__ buf, const float4 r0,
+                                        const float4 r1, Ctr<COUNT>& ct) {
+    r.o[0] = r0.x;
+    r.o[1] = r0.y;
+    r.o[2] = r0.z;
+    r.tmin = r0.w;
+    r.d[0] = r1.x;
+    r.d[1] = r1.y;
+    r.d[2] = r1.z;
+    r.tmax = r1.w;
+    tmax_finite = r.tmax < __int_as_float(0x7f800000);
+    if (p.root == 0) return false;  // empty volume: buffer [0]
+    moving = 0;
+    dneg = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (r.d[a] != 0.f) moving |= 1 << a;
+      if (r.d[a] < 0.f) dneg |= 1 << a;
       r.inv[a] = r.d[a] != 0.f ? __frcp_rn(r.d[a]) : 0.f;
     }
-    if (!moving) break;                        // reading A5: all-zero direction misses
-    if (!(r.tmin < r.tmax) && tmax_finite) break;
-    Event E{TMIN_AXIS, 0, r.tmin};
+    if (!moving) return false;  // reading A5: all-zero direction misses
+    if (!(r.tmin < r.tmax) && tmax_finite) return false;
+    E = Event{TMIN_AXIS, 0, r.tmin};
     bool miss = false;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (!((moving >> a) & 1)) {
         // half-open membership: floor(o_a) in [0, R_a)
-        if (!(r.o[a] >= 0.f && r.o[a] < (float)R[a])) miss = true;
+        if (!(r.o[a] >= 0.f && r.o[a] < (float)p.dims[a])) miss = true;
         continue;
       }
-      const int Pe = r.d[a] > 0.f ? 0 : R[a];
+      const int Pe = r.d[a] > 0.f ? 0 : p.dims[a];
       const Event Ea{a, Pe, tplane(Pe, r.o[a], r.inv[a])};
       if (cmp_ee(r, Ea, E) > 0) E = Ea;
     }
-    if (miss) break;
+    if (miss) return false;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (!((moving >> a) & 1)) continue;
-      const int Px = r.d[a] > 0.f ? R[a] : 0;
+      const int Px = r.d[a] > 0.f ? p.dims[a] : 0;
       if (cmp_ep(r, E, a, Px) >= 0) miss = true;  // entered at / after the exit of slab a
     }
-    if (miss || (tmax_finite && cmp_es(r, E, r.tmax) >= 0)) break;
-
-    // ---- entry cell (exact right limit at t_start) -------------------------------------
-    int V[3];
+    if (miss || (tmax_finite && cmp_es(r, E, r.tmax) >= 0)) return false;
 #pragma unroll
-    for (int b = 0; b < 3; ++b) V[b] = ((moving >> b) & 1) ? locate(r, E, b, 0, R[b] - 1) : (int)floorf(r.o[b]);
+    for (int b = 0; b < 3; ++b)
+      V[b] = ((moving >> b) & 1) ? locate(r, E, b, 0, p.dims[b] - 1) : (int)floorf(r.o[b]);
     ct.add(VF_CTR_LOCATES, 3);
+    set_tier(p, 0);
+    N = p.root;
+    hd = load_header<KINDS>(buf, kind, N, ct);
+    stale = 0;
+    return true;
+  }
 
-    // ---- flattened per-level traversal ---------------------------------------------------
-    const int T = (int)p.n_tiers;
-    int t = 0;
-    uint32_t N = p.root;
-    uint32_t stk[VF_MAX_TIERS];
-    uint32_t kind = p.kind_pack & 3u;
-    Header hd = load_header<KINDS>(buf, kind, N, ct);
-    int stale = 0;
-    bool hit = false;
-    // Invariant at the top of the loop: V >> lc(t) is the current (untested) cell of node N
-    // at tier t, entered at event E. A pop always follows a step, so it lands on a new cell.
-    for (;;) {
-      const uint32_t lc = field4(p.lc_pack, t);
-      {
-        // -- test the current cell of the current node (ordered_hit_children, one child)
-        const uint32_t lf = field4(p.lf_pack, t);
-        const uint32_t msk = t == 0 ? 0xFFFFFFFFu : ((1u << lf) - 1u);
-        const uint32_t lx = ((uint32_t)V[0] >> lc) & msk, ly = ((uint32_t)V[1] >> lc) & msk,
-                       lz = ((uint32_t)V[2] >> lc) & msk;
-        const uint32_t sx = t == 0 ? p.lf0[0] : lf, sxy = t == 0 ? p.lf0[0] + p.lf0[1] : 2 * lf;
-        const bool last = (p.last_mask >> t) & 1u;
-        const bool finest = t == T - 1;
-        bool occ = false;
-        uint32_t child = 0;
-        ct.add(VF_CTR_CELL_TESTS);
-        if (has_kind<KINDS>(K_RAW) && kind == K_RAW) {
-          // 64-bit index: a single-level R(11^3) grid has 2^33 cells (reading A15)
-          const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
-          child = __ldg(buf + (size_t)N + lin);
-          occ = child != 0u;
-          ct.add(VF_CTR_RAW_CELLS);
-          ct.add(VF_CTR_FORMAT_BYTES, 4);
-        } else {
-          const uint32_t lin = lx + (ly << sx) + (lz << sxy);
-          occ = (hd.mask >> lin) & 1u;
-          if (occ && !finest) {
-            const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
-            if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
-              child = hd.base + 2u * rank;
-            } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-              child = __ldg(buf + hd.base + 1u + rank);
-              ct.add(VF_CTR_SVDAG_PTRS);
-              ct.add(VF_CTR_FORMAT_BYTES, 4);
-            } else {
-              child = hd.base + (last ? 1u : 4u) * rank;
-            }
-            if (last) {  // leaf TermInt -> next level's root
-              child = __ldg(buf + child);
-              ct.add(VF_CTR_LEAF_WORDS);
-              ct.add(VF_CTR_FORMAT_BYTES, 4);
-            }
-          }
-        }
-        if (occ) {
-          if (finest) {  // unit intersection
-            hit = true;
-            break;
-          }
-          // descend at event E: make the sub-cell bits of stale axes exact
-          if (stale) {
-#pragma unroll
-            for (int b = 0; b < 3; ++b)
-              if ((stale >> b) & 1) {
-                const int lo = (V[b] >> lc) << lc;
-                V[b] = locate(r, E, b, lo, lo + (1 << lc) - 1);
-                ct.add(VF_CTR_LOCATES);
-              }
-            stale = 0;
-          }
-          if (!RESTART || ((p.top_mask >> t) & 1u)) stk[t] = N;
-          ++t;
-          N = child;
-          kind = (p.kind_pack >> (2 * t)) & 3u;
-          hd = load_header<KINDS>(buf, kind, N, ct);
-          ct.add(VF_CTR_DESCENTS);
-          continue;
-        }
-      }
-      // -- step: exact next event among the three axes at this tier's cell size
-      ct.add(VF_CTR_STEPS);
-      int Pn[3];
-      float tn[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const int c = V[a] >> lc;
-        Pn[a] = (r.d[a] > 0.f ? c + 1 : c) << lc;
-        tn[a] = ((moving >> a) & 1) ? tplane(Pn[a], r.o[a], r.inv[a]) : __int_as_float(0x7f800000);
-      }
-      const float m = fminf(fminf(tn[0], tn[1]), tn[2]);
-      const float thr = fmaf(m, kCertEps, m);
-      const int c = (tn[0] <= thr ? 1 : 0) | (tn[1] <= thr ? 2 : 0) | (tn[2] <= thr ? 4 : 0);
-      int S, a0;
-      if ((c & (c - 1)) == 0) {
-        S = c;
-        a0 = __ffs(c) - 1;
+  // Invariant: V >> lc is the current (untested) cell of node N at tier t, entered at E.
+  // A pop always follows a step, so it lands on a new cell.
+  __device__ __forceinline__ int iterate(const TraceParams& p, const uint32_t* __restrict__ buf,
+                                         uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
+    {
+      // -- test the current cell of the current node (ordered_hit_children, one child)
+      const uint32_t lx = ((uint32_t)V[0] >> lc) & msk, ly = ((uint32_t)V[1] >> lc) & msk,
+                     lz = ((uint32_t)V[2] >> lc) & msk;
+      bool occ = false;
+      uint32_t child = 0;
+      ct.add(VF_CTR_CELL_TESTS);
+      if (has_kind<KINDS>(K_RAW) && kind == K_RAW) {
+        // 64-bit index: a single-level R(11^3) grid has 2^33 cells (reading A15)
+        const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
+        child = __ldg(buf + (size_t)N + lin);
+        occ = child != 0u;
+        ct.add(VF_CTR_RAW_CELLS);
+        ct.add(VF_CTR_FORMAT_BYTES, 4);
       } else {
-        const int res = argmin_exact(r, Pn[0], Pn[1], Pn[2], tn[0], tn[1], tn[2], c);
-        S = res & 7;
-        a0 = res >> 4;
-        ct.add(VF_CTR_NEAR_TIES);
+        const uint32_t lin = lx + (ly << sx) + (lz << sxy);
+        occ = (hd.mask >> lin) & 1u;
+        if (occ && !finest) {
+          const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
+          if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
+            child = hd.base + 2u * rank;
+          } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
+            child = __ldg(buf + hd.base + 1u + rank);
+            ct.add(VF_CTR_SVDAG_PTRS);
+            ct.add(VF_CTR_FORMAT_BYTES, 4);
+          } else {
+            child = hd.base + (last ? 1u : 4u) * rank;
+          }
+          if (last) {  // leaf TermInt -> next level's root
+            child = __ldg(buf + child);
+            ct.add(VF_CTR_LEAF_WORDS);
+            ct.add(VF_CTR_FORMAT_BYTES, 4);
+          }
+        }
       }
-      E.axis = a0;
-      E.P = sel3(Pn, a0);
-      E.t = sel3(tn, a0);
-      if (tmax_finite && cmp_es(r, E, r.tmax) >= 0) break;  // segment ends (reading A7)
-      uint32_t h = 0;
+      if (occ) {
+        if (finest) return IT_HIT;  // unit intersection
+        // descend at event E: make the sub-cell bits of stale axes exact
+        if (stale) {
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            if ((stale >> b) & 1) {
+              const int lo = (V[b] >> lc) << lc;
+              V[b] = locate(r, E, b, lo, lo + (1 << lc) - 1);
+              ct.add(VF_CTR_LOCATES);
+            }
+          stale = 0;
+        }
+        if (!RESTART || ((p.top_mask >> t) & 1u)) stk[t] = N;
+        set_tier(p, t + 1);
+        N = child;
+        hd = load_header<KINDS>(buf, kind, N, ct);
+        ct.add(VF_CTR_DESCENTS);
+        return IT_CONTINUE;
+      }
+    }
+    // -- step: exact next event among the three axes at this tier's cell size
+    ct.add(VF_CTR_STEPS);
+    int Pn[3];
+    float tn[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int c = V[a] >> lc;
+      Pn[a] = (((dneg >> a) & 1) ? c : c + 1) << lc;
+      tn[a] = ((moving >> a) & 1) ? tplane(Pn[a], r.o[a], r.inv[a]) : __int_as_float(0x7f800000);
+    }
+    const float m = fminf(fminf(tn[0], tn[1]), tn[2]);
+    const float thr = fmaf(m, kCertEps, m);
+    const int c = (tn[0] <= thr ? 1 : 0) | (tn[1] <= thr ? 2 : 0) | (tn[2] <= thr ? 4 : 0);
+    int S, a0;
+    if ((c & (c - 1)) == 0) {
+      S = c;
+      a0 = __ffs(c) - 1;
+    } else {
+      const int res = argmin_exact(r.o[0], r.o[1], r.o[2], r.d[0], r.d[1], r.d[2], Pn[0], Pn[1], Pn[2], tn[0], tn[1],
+                                   tn[2], c);
+      S = res & 7;
+      a0 = res >> 4;
+      ct.add(VF_CTR_NEAR_TIES);
+    }
+    E.axis = a0;
+    E.P = sel3(Pn, a0);
+    E.t = sel3(tn, a0);
+    if (tmax_finite && cmp_es(r, E, r.tmax) >= 0) return IT_MISS;  // segment ends (reading A7)
+    uint32_t h;
+    if (S == (1 << a0)) {
+      // common case: one axis steps into the cell adjacent to plane E.P
+      const int nv = E.P - ((dneg >> a0) & 1);
+      if ((uint32_t)nv >= (uint32_t)sel3(p.dims, a0)) return IT_MISS;  // left the root box
+      h = 31u - __clz((uint32_t)(nv ^ sel3(V, a0)));
+      V[0] = a0 == 0 ? nv : V[0];
+      V[1] = a0 == 1 ? nv : V[1];
+      V[2] = a0 == 2 ? nv : V[2];
+    } else {
+      // exact tie: every axis of S steps at once (reading A2)
+      h = 0;
       bool out_of_box = false;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         if (!((S >> a) & 1)) continue;
-        const int nv = r.d[a] > 0.f ? Pn[a] : Pn[a] - 1;
-        if (nv < 0 || nv >= R[a]) out_of_box = true;
+        const int nv = Pn[a] - ((dneg >> a) & 1);
+        if (nv < 0 || nv >= p.dims[a]) out_of_box = true;
         h = max(h, 31u - __clz((uint32_t)(nv ^ V[a])));
         V[a] = nv;
       }
-      if (out_of_box) break;  // left the root box: miss
-      if (lc) stale |= ~S & moving;
-      stale &= ~S;
-      const int tau = (int)field4(p.tau_pack, h);
-      if (tau < t) {
-        ct.add(VF_CTR_POPS);
-        // left the current node: pop (stack) or restart from the level root
-        if (!RESTART) {
-          t = tau;
-          N = stk[t];
-          kind = (p.kind_pack >> (2 * t)) & 3u;
-          hd = load_header<KINDS>(buf, kind, N, ct);
-        } else {
-          const int top = (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tau);
-          t = top;
-          N = stk[t];
-          kind = (p.kind_pack >> (2 * t)) & 3u;
-          hd = load_header<KINDS>(buf, kind, N, ct);
-          while (t < tau) {  // re-descend through nodes that contain the current cell
-            const uint32_t lct = field4(p.lc_pack, t), lf = field4(p.lf_pack, t);
-            const uint32_t msk = t == 0 ? 0xFFFFFFFFu : ((1u << lf) - 1u);
-            const uint32_t lin = (((uint32_t)V[0] >> lct) & msk) +
-                                 ((((uint32_t)V[1] >> lct) & msk) << (t == 0 ? p.lf0[0] : lf)) +
-                                 ((((uint32_t)V[2] >> lct) & msk) << (t == 0 ? p.lf0[0] + p.lf0[1] : 2 * lf));
-            const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
-            uint32_t child;
-            if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
-              child = hd.base + 2u * rank;
-            } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-              child = __ldg(buf + hd.base + 1u + rank);
-              ct.add(VF_CTR_SVDAG_PTRS);
-              ct.add(VF_CTR_FORMAT_BYTES, 4);
-            } else {
-              child = hd.base + 4u * rank;  // N^3 internal (t < tau <= last tier of the level)
-            }
-            ++t;
-            N = child;
-            kind = (p.kind_pack >> (2 * t)) & 3u;
-            hd = load_header<KINDS>(buf, kind, N, ct);
-            ct.add(VF_CTR_REDESCENTS);
+      if (out_of_box) return IT_MISS;  // left the root box
+    }
+    if (lc) stale |= ~S & moving;
+    stale &= ~S;
+    const int tau = (int)field4(p.tau_pack, h);
+    if (tau < t) {
+      ct.add(VF_CTR_POPS);
+      // left the current node: pop (stack) or restart from the level root
+      if (!RESTART) {
+        set_tier(p, tau);
+        N = stk[tau];
+        hd = load_header<KINDS>(buf, kind, N, ct);
+      } else {
+        const int top = (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tau);
+        set_tier(p, top);
+        N = stk[top];
+        hd = load_header<KINDS>(buf, kind, N, ct);
+        while (t < tau) {  // re-descend through nodes that contain the current cell
+          const uint32_t lin = (((uint32_t)V[0] >> lc) & msk) + ((((uint32_t)V[1] >> lc) & msk) << sx) +
+                               ((((uint32_t)V[2] >> lc) & msk) << sxy);
+          const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
+          uint32_t child;
+          if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
+            child = hd.base + 2u * rank;
+          } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
+            child = __ldg(buf + hd.base + 1u + rank);
+            ct.add(VF_CTR_SVDAG_PTRS);
+            ct.add(VF_CTR_FORMAT_BYTES, 4);
+          } else {
+            child = hd.base + 4u * rank;  // N^3 internal (t < tau <= last tier of the level)
           }
+          set_tier(p, t + 1);
+          N = child;
+          hd = load_header<KINDS>(buf, kind, N, ct);
+          ct.add(VF_CTR_REDESCENTS);
         }
       }
     }
-    if (hit) {
-      out = make_int4(V[0], V[1], V[2], __float_as_int(E.t));
-      ct.add(VF_CTR_HITS);
+    return IT_CONTINUE;
+  }
+
+  __device__ __forceinline__ int4 hit_record() const { return make_int4(V[0], V[1], V[2], __float_as_int(E.t)); }
+};
+
+__device__ __forceinline__ int4 miss_record() { return make_int4(-1, -1, -1, 0x7f800000); }
+
+// One thread per ray, one launch wave per 256 rays.
+template <uint32_t KINDS, bool RESTART, bool COUNT>
+__global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
+                                                    const float4* __restrict__ rays, int4* __restrict__ hits,
+                                                    uint64_t n, unsigned long long* __restrict__ counters,
+                                                    unsigned long long* __restrict__ work) {
+  const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  Ctr<COUNT> ct;
+  if (gid < n) {
+    Lane<KINDS, RESTART, COUNT> L;
+    uint32_t stk[VF_MAX_TIERS];
+    int4 out = miss_record();
+    if (L.start(p, buf, __ldg(rays + 2 * gid), __ldg(rays + 2 * gid + 1), ct)) {
+      int res;
+      do {
+        res = L.iterate(p, buf, stk, ct);
+      } while (res == IT_CONTINUE);
+      if (res == IT_HIT) {
+        out = L.hit_record();
+        ct.add(VF_CTR_HITS);
+      }
     }
-  } while (0);
-  hits[gid] = out;
-  ct.add(VF_CTR_RAYS);
+    hits[gid] = out;
+    ct.add(VF_CTR_RAYS);
   }
   ct.flush(counters);
+}
+
+// Persistent warps with dynamic ray fetch: grid = resident blocks; a warp keeps its lanes busy
+// by fetching a new batch of rays (one atomicAdd per batch) whenever at least kRefill lanes have
+// finished. This removes the SIMT loss of finished lanes idling until the slowest ray of the
+// warp ends, and the launch tail (SURVEY.md §8(d) "warp ballot early-out / persistent refill").
+// work[0] = next ray, work[1] = finished blocks; the last block resets both.
+constexpr int kPersistThreads = 128;
+
+template <uint32_t KINDS, bool RESTART, bool COUNT>
+__global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceParams p, const uint32_t* __restrict__ buf,
+                                                                   const float4* __restrict__ rays,
+                                                                   int4* __restrict__ hits, uint64_t n,
+                                                                   unsigned long long* __restrict__ counters,
+                                                                   unsigned long long* __restrict__ work) {
+  Ctr<COUNT> ct;
+  Lane<KINDS, RESTART, COUNT> L;
+  uint32_t stk[VF_MAX_TIERS];
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned lt = (1u << lane) - 1u;
+  bool active = false, exhausted = false;
+  uint64_t idx = 0;
+  for (;;) {
+    unsigned idle = __ballot_sync(0xffffffffu, !active);
+    if (!exhausted && __popc(idle) >= p.refill) {
+      unsigned long long base = 0;
+      const unsigned cnt = __popc(idle);
+      if (lane == 0) base = atomicAdd(work, (unsigned long long)cnt);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base + cnt >= n) exhausted = true;
+      if (!active) {
+        idx = base + __popc(idle & lt);
+        if (idx < n) {
+          ct.add(VF_CTR_RAYS);
+          if (L.start(p, buf, __ldg(rays + 2 * idx), __ldg(rays + 2 * idx + 1), ct))
+            active = true;
+          else
+            hits[idx] = miss_record();
+        }
+      }
+      idle = __ballot_sync(0xffffffffu, !active);
+    }
+    if (idle == 0xffffffffu) {
+      if (exhausted) break;
+      continue;
+    }
+    if (active) {
+      const int res = L.iterate(p, buf, stk, ct);
+      if (res != IT_CONTINUE) {
+        if (res == IT_HIT) ct.add(VF_CTR_HITS);
+        hits[idx] = res == IT_HIT ? L.hit_record() : miss_record();
+        active = false;
+      }
+    }
+  }
+  ct.flush(counters);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long done = atomicAdd(work + 1, 1ull);
+    if (done == gridDim.x - 1) {  // last block: reset the work counter for the next launch
+      atomicExch(work, 0ull);
+      atomicExch(work + 1, 0ull);
+    }
+  }
 }
 
 // ---- point query: integer-only descent (test aid) ------------------------------------------
@@ -541,25 +696,49 @@ __global__ void query_kernel(const TraceParams p, const uint32_t* __restrict__ b
   }
 }
 
-using KernelFn = void (*)(const TraceParams, const uint32_t*, const float4*, int4*, uint64_t, unsigned long long*);
+using KernelFn = void (*)(const TraceParams, const uint32_t*, const float4*, int4*, uint64_t, unsigned long long*,
+                          unsigned long long*);
+
+template <uint32_t K, bool R, bool C>
+KernelFn pick(bool persistent) {
+  return persistent ? trace_persistent<K, R, C> : trace_kernel<K, R, C>;
+}
 
 template <uint32_t K>
-struct Table {
-  static KernelFn get(bool restart, bool count) {
-    if (count) return restart ? trace_kernel<K, true, true> : trace_kernel<K, false, true>;
-    return restart ? trace_kernel<K, true, false> : trace_kernel<K, false, false>;
-  }
-};
+KernelFn get_kernel(bool restart, bool count, bool persistent) {
+  if (count) return restart ? pick<K, true, true>(persistent) : pick<K, false, true>(persistent);
+  return restart ? pick<K, true, false>(persistent) : pick<K, false, false>(persistent);
+}
 
-KernelFn select_kernel(uint32_t kinds, bool restart, bool count) {
+KernelFn select_kernel(uint32_t kinds, bool restart, bool count, bool persistent) {
   switch (kinds) {
 #define VF_CASE(k) \
-  case k: return Table<k>::get(restart, count);
+  case k: return get_kernel<k>(restart, count, persistent);
     VF_CASE(1) VF_CASE(2) VF_CASE(3) VF_CASE(4) VF_CASE(5) VF_CASE(6) VF_CASE(7) VF_CASE(8) VF_CASE(9) VF_CASE(10)
     VF_CASE(11) VF_CASE(12) VF_CASE(13) VF_CASE(14) VF_CASE(15)
 #undef VF_CASE
     default: return nullptr;
   }
+}
+
+// resident blocks per SM for a persistent kernel (cached per function and device)
+int persistent_blocks(KernelFn fn, int device) {
+  struct Entry {
+    KernelFn fn;
+    int dev, blocks;
+  };
+  static Entry cache[256];
+  static int n_cache = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  for (int i = 0; i < n_cache; ++i)
+    if (cache[i].fn == fn && cache[i].dev == device) return cache[i].blocks;
+  int per_sm = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPersistThreads, 0);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  int blocks = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+  if (n_cache < 256) cache[n_cache++] = Entry{fn, device, blocks};
+  return blocks;
 }
 
 }  // namespace
@@ -569,19 +748,39 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
   if (n == 0) return VF_OK;
   uint32_t kinds = 0;
   for (uint32_t t = 0; t < h->fmt.n_tiers; ++t) kinds |= 1u << h->fmt.tiers[t].kind;
-  KernelFn fn = select_kernel(kinds, (flags & VF_TRACE_RESTART_SV) != 0, counters != nullptr);
+  const bool persistent = (flags & VF_TRACE_PERSISTENT_WARPS) != 0;
+  KernelFn fn = select_kernel(kinds, (flags & VF_TRACE_RESTART_SV) != 0, counters != nullptr, persistent);
   if (!fn) {
     set_error("vf_trace: no kernel instantiated for kind set 0x%x", kinds);
     return VF_ERR_UNSUPPORTED;
   }
-  const unsigned threads = 256;
-  const uint64_t blocks = (n + threads - 1) / threads;
-  if (blocks > 0x7fffffffull) {
-    set_error("vf_trace: %llu rays exceed one launch", (unsigned long long)n);
-    return VF_ERR_INVALID_ARG;
+  if (persistent) {
+    static const int refill_env = [] {
+      const char* e = getenv("VF_REFILL");
+      const int v = e ? atoi(e) : 0;
+      return (v >= 1 && v <= 32) ? v : 0;
+    }();
+    TraceParams tp = h->tp;
+    if (refill_env) tp.refill = (uint32_t)refill_env;
+    const uint32_t slot = h->work_slot.fetch_add(1) % kWorkSlots;
+    unsigned long long* work = h->work + 2 * slot;
+    const int blocks = persistent_blocks(fn, h->device);
+    fn<<<blocks, kPersistThreads, 0, s>>>(tp, h->buf, reinterpret_cast<const float4*>(rays),
+                                          reinterpret_cast<int4*>(hits), n, counters, work);
+  } else {
+    static const unsigned threads = [] {
+      const char* e = getenv("VF_BLOCK");
+      const int v = e ? atoi(e) : 0;
+      return (v == 32 || v == 64 || v == 128 || v == 256) ? (unsigned)v : 128u;
+    }();
+    const uint64_t blocks = (n + threads - 1) / threads;
+    if (blocks > 0x7fffffffull) {
+      set_error("vf_trace: %llu rays exceed one launch", (unsigned long long)n);
+      return VF_ERR_INVALID_ARG;
+    }
+    fn<<<(unsigned)blocks, threads, 0, s>>>(h->tp, h->buf, reinterpret_cast<const float4*>(rays),
+                                            reinterpret_cast<int4*>(hits), n, counters, nullptr);
   }
-  fn<<<(unsigned)blocks, threads, 0, s>>>(h->tp, h->buf, reinterpret_cast<const float4*>(rays),
-                                          reinterpret_cast<int4*>(hits), n, counters);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("vf_trace: launch failed: %s", cudaGetErrorString(e));

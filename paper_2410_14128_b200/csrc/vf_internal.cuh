@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "../../include/vf.h"
@@ -50,7 +51,7 @@ struct TraceParams {
   uint32_t kind_pack;   // 2 bits per tier
   uint32_t top_mask;    // bit t: tier t is its level's top
   uint32_t last_mask;   // bit t: tier t is its level's last tier
-  uint32_t top_of;      // unused (reserved)
+  uint32_t refill;      // persistent trace: refill a warp when >= refill lanes are idle
   uint32_t lf0[3];      // tier-0 fan-out per axis (log2)
   int32_t dims[3];      // resolution per axis
   uint32_t n_tiers;
@@ -69,7 +70,14 @@ struct Handle {
   // staging for vf_trace_host
   void* stage = nullptr;
   size_t stage_bytes = 0;
+  // persistent-trace work counters: kWorkSlots x {next ray, finished blocks}, self-resetting
+  unsigned long long* work = nullptr;
+  mutable std::atomic<uint32_t> work_slot{0};
 };
+
+constexpr uint32_t kWorkSlots = 64;
+// internal trace flag (ablation / tests): persistent warps with dynamic ray refill
+constexpr uint32_t VF_TRACE_PERSISTENT_WARPS = 1u << 30;
 
 // errors
 void set_error(const char* fmt, ...);

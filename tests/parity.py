@@ -10,10 +10,10 @@ import numpy as np
 T_RTOL = 1e-4
 
 
-def gpu_trace(handle, rays_np, restart=False):
+def gpu_trace(handle, rays_np, restart=False, persistent=False):
     import torch
     r = torch.from_numpy(np.ascontiguousarray(rays_np, dtype=np.float32)).cuda()
-    h = handle.trace(r, restart=restart)
+    h = handle.trace(r, restart=restart, persistent=persistent)
     torch.cuda.synchronize()
     out = h.cpu().numpy()
     xyz = out[:, :3].astype(np.int32)

@@ -67,8 +67,9 @@ def test_small_formats_vs_oracle(fmt, p):
     rays = _rays_small(dims, 99)
     ref = oracle.Grid.from_generator(d).trace(rays)
     for restart in (False, True):
-        xyz, t = gpu_trace(h, rays, restart)
-        assert_parity(xyz, t, ref, f"{fmt} p={p} restart={restart}")
+        for pers in (False, True):
+            xyz, t = gpu_trace(h, rays, restart, pers)
+            assert_parity(xyz, t, ref, f"{fmt} p={p} restart={restart} persistent={pers}")
 
 
 @pytest.mark.parametrize("fmt,dims", [
@@ -181,6 +182,31 @@ def test_format_errors():
     with pytest.raises(vf.VfError) as e:
         vf.build(v, "G(5)")
     assert e.value.status == vf.VF_ERR_FORMAT
+
+
+def test_counters_consistent():
+    """The counting variant returns the same hits and sane per-ray work counts."""
+    import torch
+    vf = _vf()
+    d = inputs.menger(256, 5)
+    keys, rgba = inputs.voxels_device(d)
+    rays, _ = R.camera("menger", scale=4)
+    rt = torch.from_numpy(rays).cuda()
+    for fmt, fields in [("G(5) R(3, 3, 3)", ("svdag_nodes", "raw_cells")), ("S(8)", ("svo_nodes",)),
+                        ("T(2, 4)", ("ntree_nodes",))]:
+        h = vf.build((keys, rgba, (256, 256, 256)), fmt)
+        a = h.trace(rt).cpu().numpy()
+        hits = torch.empty_like(rt[:, :4].contiguous().view(torch.int32))
+        c = h.counters(rt, hits)
+        np.testing.assert_array_equal(hits.cpu().numpy(), a)
+        n = len(rays)
+        assert c["rays"] == n and c["hits"] == int((a[:, 0] >= 0).sum())
+        for f in fields:
+            assert c[f] > 0
+        per = 4 * (c["raw_cells"] + c["svdag_nodes"] + c["svdag_ptrs"] + c["leaf_words"]) + 8 * c["svo_nodes"] + \
+            16 * c["ntree_nodes"]
+        assert c["format_bytes"] == per
+        assert c["exact_calls"] < 0.05 * n
 
 
 def test_trace_host_matches_device():

@@ -1,0 +1,78 @@
+"""World-size-2 CPU (gloo) test of the multi-GPU host logic: interleaved screen-tile sharding,
+the one hit-gather collective and the un-permutation on rank 0."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import torch.multiprocessing as mp
+
+from inputs import rays as R
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, width, height, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2410_14128_b200 import shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    perm = R.tile_order(width, height)
+    own = shard.shard(perm, width, rank, world)
+    # stand-in for vf_trace: a hit record that encodes the pixel it belongs to
+    pix = perm[own]
+    hits = torch.from_numpy(np.stack([pix, pix * 3, -pix, pix % 7], 1).astype(np.int32))
+    counts = shard.shard_counts(perm, width, world)
+    bufs = shard.gather_hits(hits, counts)
+    if rank == 0:
+        img = shard.assemble(bufs, perm, width, world)
+        q.put(img)
+    dist.destroy_process_group()
+
+
+def test_tile_shard_gather_unpermute_gloo():
+    width, height, world = 72, 40, 2  # ragged: tiles at the right/bottom edge are partial
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, width, height, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    img = q.get(timeout=120)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    pix = np.arange(width * height)
+    np.testing.assert_array_equal(img[:, 0], pix)
+    np.testing.assert_array_equal(img[:, 1], pix * 3)
+    np.testing.assert_array_equal(img[:, 2], -pix)
+    np.testing.assert_array_equal(img[:, 3], pix % 7)
+
+
+def test_shards_partition_and_balance():
+    from paper_2410_14128_b200 import shard
+    perm = R.tile_order(1920, 1080)
+    for world in (1, 2, 4, 8):
+        parts = [shard.shard(perm, 1920, r, world) for r in range(world)]
+        allidx = np.sort(np.concatenate(parts))
+        np.testing.assert_array_equal(allidx, np.arange(len(perm)))
+        sizes = [len(p) for p in parts]
+        assert max(sizes) / (sum(sizes) / world) < 1.03  # interleaved tiles: balanced ray counts
+        assert sizes == shard.shard_counts(perm, 1920, world)
+
+
+def test_tile_order_is_a_permutation_with_warp_tiles():
+    perm = R.tile_order(64, 48)
+    assert sorted(perm.tolist()) == list(range(64 * 48))
+    # the first 32 rays form one 8x4 warp tile
+    px, py = perm[:32] % 64, perm[:32] // 64
+    assert px.max() - px.min() == 7 and py.max() - py.min() == 3
