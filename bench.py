@@ -129,7 +129,7 @@ def cpu_baseline(vol_desc, rays, gpu_xyz, gpu_t, budget_s=12.0):
     same frame; also checks parity of the sampled rays against the GPU hits."""
     import oracle
     from parity import compare
-    g = oracle.Grid.procedural(vol_desc) if vol_desc.gen != 5 else oracle.Grid.from_generator(vol_desc)
+    g = oracle.Grid.procedural(vol_desc)
     cores = oracle.max_threads()
     n = len(rays)
     m = min(n, 2048)
@@ -364,7 +364,7 @@ def run_reference(args):
     vname, _, deffmt, desc = CONFIGS[cfg]
     vol = make_volume(vname)
     rays_all, _ = make_rays(cfg)
-    g = oracle.Grid.procedural(vol) if vol.gen != 5 else oracle.Grid.from_generator(vol)
+    g = oracle.Grid.procedural(vol)
     cores = oracle.max_threads()
     n = len(rays_all)
     m = 4096

@@ -53,7 +53,18 @@ typedef struct {
   uint64_t* bits; /* bit (x + Rx*(y + Ry*z)) set iff voxel non-empty */
   int owns_gen;   /* procedural mode: evaluate volgen per visited cell, no bitset */
   vg_desc gen;
+  /* procedural G5: objects binned by 64^3 cells of their AABB [c-r, c+r) */
+  int64_t nb[3];
+  uint32_t* bin_start; /* CSR over bins */
+  vg_object* bin_obj;
 } oracle_grid;
+
+static int sparse_occupied(const oracle_grid* g, int64_t x, int64_t y, int64_t z) {
+  const uint64_t b = (uint64_t)(x >> 6) + (uint64_t)g->nb[0] * ((uint64_t)(y >> 6) + (uint64_t)g->nb[1] * (uint64_t)(z >> 6));
+  for (uint32_t i = g->bin_start[b]; i < g->bin_start[b + 1]; ++i)
+    if (vg_object_contains(&g->bin_obj[i], x, y, z)) return 1;
+  return 0;
+}
 
 static inline uint64_t lin(const oracle_grid* g, int64_t x, int64_t y, int64_t z) {
   return (uint64_t)x + (uint64_t)g->dims[0] * ((uint64_t)y + (uint64_t)g->dims[1] * (uint64_t)z);
@@ -64,6 +75,7 @@ static inline int occupied(const oracle_grid* g, int64_t x, int64_t y, int64_t z
     uint64_t i = lin(g, x, y, z);
     return (int)((g->bits[i >> 6] >> (i & 63)) & 1u);
   }
+  if (g->bin_start) return sparse_occupied(g, x, y, z);
   return vg_voxel(&g->gen, x, y, z) != 0;
 }
 
@@ -131,18 +143,68 @@ oracle_grid* oracle_grid_from_generator(const vg_desc* d, int nthreads) {
 /* Procedural occupancy (no bitset): bit(cell) = vg_voxel(cell) != 0. Same definition,
  * used for sampled parity at sizes whose bitset is too large to build in a test. */
 oracle_grid* oracle_grid_procedural(const vg_desc* d) {
-  if (d->gen == VG_SPARSE) return NULL; /* needs the object table: use the bitset */
   oracle_grid* g = (oracle_grid*)calloc(1, sizeof(oracle_grid));
   if (!g) return NULL;
   for (int a = 0; a < 3; ++a) g->dims[a] = d->dims[a];
   g->owns_gen = 1;
   g->gen = *d;
+  if (d->gen == VG_SPARSE) {
+    /* occupancy = union of the object shells (colour irrelevant): bin every object into the
+     * 64^3 cells its AABB touches, two passes (count, fill) */
+    for (int a = 0; a < 3; ++a) g->nb[a] = (g->dims[a] + 63) / 64;
+    const uint64_t nbins = (uint64_t)g->nb[0] * g->nb[1] * g->nb[2];
+    g->bin_start = (uint32_t*)calloc(nbins + 1, sizeof(uint32_t));
+    if (!g->bin_start) {
+      free(g);
+      return NULL;
+    }
+    for (int pass = 0; pass < 2; ++pass) {
+      uint32_t* fill = NULL;
+      if (pass == 1) {
+        for (uint64_t b = 0; b < nbins; ++b) g->bin_start[b + 1] += g->bin_start[b];
+        g->bin_obj = (vg_object*)malloc(sizeof(vg_object) * (g->bin_start[nbins] + 1));
+        fill = (uint32_t*)calloc(nbins, sizeof(uint32_t));
+        if (!g->bin_obj || !fill) {
+          free(fill);
+          free(g->bin_obj);
+          free(g->bin_start);
+          free(g);
+          return NULL;
+        }
+      }
+      for (uint32_t k = 0; k < VG_SPARSE_OBJECTS; ++k) {
+        vg_object o = vg_sparse_object(k, d->seed);
+        int64_t lo[3], hi[3];
+        int ok = 1;
+        for (int a = 0; a < 3; ++a) {
+          lo[a] = o.c[a] - o.r;
+          hi[a] = o.c[a] + o.r - 1;
+          if (lo[a] < 0) lo[a] = 0;
+          if (hi[a] > g->dims[a] - 1) hi[a] = g->dims[a] - 1;
+          if (hi[a] < lo[a]) ok = 0;
+        }
+        if (!ok) continue;
+        for (int64_t bz = lo[2] >> 6; bz <= hi[2] >> 6; ++bz)
+          for (int64_t by = lo[1] >> 6; by <= hi[1] >> 6; ++by)
+            for (int64_t bx = lo[0] >> 6; bx <= hi[0] >> 6; ++bx) {
+              const uint64_t b = (uint64_t)bx + (uint64_t)g->nb[0] * ((uint64_t)by + (uint64_t)g->nb[1] * (uint64_t)bz);
+              if (pass == 0)
+                g->bin_start[b + 1]++;
+              else
+                g->bin_obj[g->bin_start[b] + fill[b]++] = o;
+            }
+      }
+      free(fill);
+    }
+  }
   return g;
 }
 
 void oracle_grid_free(oracle_grid* g) {
   if (!g) return;
   free(g->bits);
+  free(g->bin_start);
+  free(g->bin_obj);
   free(g);
 }
 

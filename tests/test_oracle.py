@@ -232,3 +232,13 @@ def test_sparse_rasteriser_matches_generator():
         assert inputs.voxel_host(d, x, y, z) != 0   # brute-force lowest-k definition
     for x, y, z in rng.integers(0, 384, size=(300, 3)):
         assert g.get(x, y, z) == (inputs.voxel_host(d, x, y, z) != 0) == bool(dense[z, y, x])
+
+
+def test_procedural_sparse_equals_bitset():
+    d = inputs.sparse(384, 0x4096)
+    rays = np.concatenate([R.random_rays(6000, (384,) * 3, 3), R.adversarial_rays(2000, (384,) * 3, 4)])
+    a = oracle.Grid.from_generator(d).trace(rays)
+    b = oracle.Grid.procedural(d).trace(rays)
+    assert (a["status"] == 1).sum() > 50
+    np.testing.assert_array_equal(a["xyz"], b["xyz"])
+    np.testing.assert_array_equal(a["t"], b["t"])
