@@ -187,6 +187,7 @@ enum {
   VF_CTR_LEAF_WORDS,    /* leaf terminating integers read (4 B) */
   VF_CTR_FORMAT_BYTES,  /* sum of the above in bytes */
   VF_CTR_EXACT_CALLS,   /* exact fallbacks (device-global counter) */
+  VF_CTR_WARP_MAX_TESTS, /* sum over warps of 32 x (max cell tests of a lane): SIMT bound */
   VF_NCOUNTERS
 };
 

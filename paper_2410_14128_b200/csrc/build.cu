@@ -529,13 +529,16 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
       return VF_ERR_OVERFLOW;
     }
     // ---- assemble: word 0 = root pointer, then each tier at its base
+    // 8 zero guard words after the last word: the trace kernel reads SVDAG headers as two
+    // 16-B vectors that may extend up to 7 words past a node
+    const uint64_t alloc_words = cursor + 8;
     uint32_t* buf = nullptr;
-    cudaError_t e = cudaMalloc(&buf, cursor * sizeof(uint32_t));
+    cudaError_t e = cudaMalloc(&buf, alloc_words * sizeof(uint32_t));
     if (e != cudaSuccess) {
       set_error("vf_build: cudaMalloc(%llu bytes) failed: %s", (unsigned long long)(cursor * 4), cudaGetErrorString(e));
       return VF_ERR_OOM;
     }
-    VF_CUDA_TRY(cudaMemsetAsync(buf, 0, cursor * sizeof(uint32_t), s));
+    VF_CUDA_TRY(cudaMemsetAsync(buf, 0, alloc_words * sizeof(uint32_t), s));
     VF_CUDA_TRY(cudaMemcpyAsync(buf, &root, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
     for (uint32_t t = 0; t < f.n_tiers; ++t)
       if (!tier_words[t].empty())

@@ -243,10 +243,28 @@ __device__ __forceinline__ bool has_kind(uint32_t k) {
 }
 
 // Node header registers for the current tier.
+#ifndef VF_SVDAG_WIDE
+#define VF_SVDAG_WIDE 0  // 1: 2 x LDG.128 SVDAG headers (A/B: slower, +50 registers)
+#endif
 struct Header {
   uint64_t mask;  // SVO/SVDAG: valid bits; N^3: 64-bit occupancy
   uint32_t base;  // SVO: first child; SVDAG: node address; N^3: children block
+#if VF_SVDAG_WIDE
+  // SVDAG: the two 16-B-aligned vectors covering the node header (paper layout, unpadded) —
+  // header at word k = N & 3, child pointers at k+1 .. 7 are then already in registers.
+  uint4 a, b;
+  uint32_t k;
+#endif
 };
+
+#if VF_SVDAG_WIDE
+// v[i] of the eight words {a.x..a.w, b.x..b.w}, i in [0, 8), without indexed memory.
+__device__ __forceinline__ uint32_t sel8(const uint4& a, const uint4& b, uint32_t i) {
+  const uint4 v = (i & 4u) ? b : a;
+  const uint32_t lo = (i & 1u) ? v.y : v.x, hi = (i & 1u) ? v.w : v.z;
+  return (i & 2u) ? hi : lo;
+}
+#endif
 
 // Per-ray work counters of the VF_COUNTERS variant (SURVEY.md §8(d) "Counts come from a
 // -DVF_COUNTERS build of the same kernel"). Compiled away when COUNT == false.
@@ -264,6 +282,7 @@ struct Ctr {
   __device__ __forceinline__ void flush(unsigned long long* out) {
     if constexpr (COUNT) {
 #pragma unroll
+      v[VF_CTR_WARP_MAX_TESTS] = 32u * __reduce_max_sync(0xffffffffu, v[VF_CTR_CELL_TESTS]);
       for (int i = 0; i < VF_NCOUNTERS; ++i) {
         unsigned long long x = v[i];
         for (int o = 16; o; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
@@ -286,7 +305,15 @@ __device__ __forceinline__ Header load_header(const uint32_t* __restrict__ buf, 
     ct.add(VF_CTR_SVO_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 8);
   } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
+#if VF_SVDAG_WIDE
+    const uint4* q = reinterpret_cast<const uint4*>(buf + (N & ~3u));
+    h.a = __ldg(q);
+    h.b = __ldg(q + 1);  // the buffer carries 8 guard words, so this never reads past the end
+    h.k = N & 3u;
+    h.mask = sel8(h.a, h.b, h.k) & 0xFFu;
+#else
     h.mask = __ldg(buf + N) & 0xFFu;
+#endif
     ct.add(VF_CTR_SVDAG_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 4);
   } else if (has_kind<KINDS>(K_NTREE) && kind == K_NTREE) {
@@ -417,7 +444,12 @@ struct Lane {
           if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
             child = hd.base + 2u * rank;
           } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
+#if VF_SVDAG_WIDE
+            const uint32_t i = hd.k + 1u + rank;
+            child = i < 8u ? sel8(hd.a, hd.b, i) : __ldg(buf + hd.base + 1u + rank);
+#else
             child = __ldg(buf + hd.base + 1u + rank);
+#endif
             ct.add(VF_CTR_SVDAG_PTRS);
             ct.add(VF_CTR_FORMAT_BYTES, 4);
           } else {
@@ -525,7 +557,12 @@ struct Lane {
           if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
             child = hd.base + 2u * rank;
           } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
+#if VF_SVDAG_WIDE
+            const uint32_t i = hd.k + 1u + rank;
+            child = i < 8u ? sel8(hd.a, hd.b, i) : __ldg(buf + hd.base + 1u + rank);
+#else
             child = __ldg(buf + hd.base + 1u + rank);
+#endif
             ct.add(VF_CTR_SVDAG_PTRS);
             ct.add(VF_CTR_FORMAT_BYTES, 4);
           } else {
@@ -546,9 +583,13 @@ struct Lane {
 
 __device__ __forceinline__ int4 miss_record() { return make_int4(-1, -1, -1, 0x7f800000); }
 
-// One thread per ray, one launch wave per 256 rays.
+// One thread per ray, 128-thread blocks.
+#ifndef VF_MINB
+#define VF_MINB 8  // __launch_bounds__ min blocks per SM (register cap), A/B-tuned
+#endif
+constexpr unsigned kTraceThreads = 128;
 template <uint32_t KINDS, bool RESTART, bool COUNT>
-__global__ void __launch_bounds__(256) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
+__global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
                                                     uint64_t n, unsigned long long* __restrict__ counters,
                                                     unsigned long long* __restrict__ work) {
@@ -771,7 +812,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     static const unsigned threads = [] {
       const char* e = getenv("VF_BLOCK");
       const int v = e ? atoi(e) : 0;
-      return (v == 32 || v == 64 || v == 128 || v == 256) ? (unsigned)v : 128u;
+      return (v == 32 || v == 64 || v == 128) ? (unsigned)v : kTraceThreads;
     }();
     const uint64_t blocks = (n + threads - 1) / threads;
     if (blocks > 0x7fffffffull) {

@@ -11,7 +11,7 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libvf.so")
+LIB_PATH = os.environ.get("VF_LIB") or os.path.join(PKG, "libvf.so")  # VF_LIB: A/B builds (tools)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (or python -m "
@@ -32,7 +32,7 @@ VF_MAX_LEVELS = 16
 VF_MAX_TIERS = 16
 COUNTER_NAMES = ("rays", "hits", "cell_tests", "steps", "descents", "pops", "redescents", "locates", "near_ties",
                  "raw_cells", "svo_nodes", "svdag_nodes", "svdag_ptrs", "ntree_nodes", "leaf_words", "format_bytes",
-                 "exact_calls")
+                 "exact_calls", "warp_max_tests")
 VF_NCOUNTERS = len(COUNTER_NAMES)
 
 
