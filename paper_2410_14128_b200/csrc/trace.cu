@@ -281,8 +281,9 @@ struct Ctr {
   }
   __device__ __forceinline__ void flush(unsigned long long* out) {
     if constexpr (COUNT) {
+      const uint32_t wmax = __reduce_max_sync(0xffffffffu, v[VF_CTR_CELL_TESTS]);
+      v[VF_CTR_WARP_MAX_TESTS] = (threadIdx.x & 31) == 0 ? 32u * wmax : 0u;
 #pragma unroll
-      v[VF_CTR_WARP_MAX_TESTS] = 32u * __reduce_max_sync(0xffffffffu, v[VF_CTR_CELL_TESTS]);
       for (int i = 0; i < VF_NCOUNTERS; ++i) {
         unsigned long long x = v[i];
         for (int o = 16; o; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
@@ -341,7 +342,8 @@ struct Lane {
   uint32_t N;     // current node (word address)
   uint32_t kind;  // kind of tier t
   Header hd;
-  int stale;   // axes whose sub-cell bits are not exact at E
+  int stale;   // axes whose bits below stale_lc are not exact at E
+  uint32_t stale_lc;  // bits of V below this are stale on the axes in `stale`
   int moving;  // axes with d != 0
   int dneg;    // axes with d < 0
   bool tmax_finite;
@@ -415,6 +417,7 @@ struct Lane {
     N = p.root;
     hd = load_header<KINDS>(buf, kind, N, ct);
     stale = 0;
+    stale_lc = 0;
     return true;
   }
 
@@ -422,6 +425,8 @@ struct Lane {
   // A pop always follows a step, so it lands on a new cell.
   __device__ __forceinline__ int iterate(const TraceParams& p, const uint32_t* __restrict__ buf,
                                          uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
+    int nt = t;       // tier after this iteration
+    uint32_t nN = N;  // node after this iteration
     {
       // -- test the current cell of the current node (ordered_hit_children, one child)
       const uint32_t lx = ((uint32_t)V[0] >> lc) & msk, ly = ((uint32_t)V[1] >> lc) & msk,
@@ -464,8 +469,10 @@ struct Lane {
       }
       if (occ) {
         if (finest) return IT_HIT;  // unit intersection
-        // descend at event E: make the sub-cell bits of stale axes exact
-        if (stale) {
+        // descend at event E. The child cell needs V's bits >= lc(t+1); if some of those are
+        // stale (the ray moved inside a cell of size 2^stale_lc since they were exact), derive the
+        // exact finest voxel of the stale axes within the current cell (bits >= lc are exact).
+        if (stale && lc - field4(p.lf_pack, t + 1) < stale_lc) {
 #pragma unroll
           for (int b = 0; b < 3; ++b)
             if ((stale >> b) & 1) {
@@ -474,16 +481,29 @@ struct Lane {
               ct.add(VF_CTR_LOCATES);
             }
           stale = 0;
+          stale_lc = 0;
         }
         if (!RESTART || ((p.top_mask >> t) & 1u)) stk[t] = N;
-        set_tier(p, t + 1);
-        N = child;
-        hd = load_header<KINDS>(buf, kind, N, ct);
+        nt = t + 1;
+        nN = child;
         ct.add(VF_CTR_DESCENTS);
-        return IT_CONTINUE;
       }
     }
-    // -- step: exact next event among the three axes at this tier's cell size
+    if (nt == t) step(p, buf, stk, ct, nt, nN);
+    if (nt < 0) return IT_MISS;
+    // tier change (descent or pop), shared by both paths so a warp mixing them runs it once
+    if (nt != t) {
+      set_tier(p, nt);
+      N = nN;
+      hd = load_header<KINDS>(buf, kind, N, ct);
+    }
+    return IT_CONTINUE;
+  }
+
+  // -- step: exact next event among the three axes at this tier's cell size. Sets nt < 0 when
+  // the segment ends (miss), nt < t (with nN) when the step leaves the current node.
+  __device__ __forceinline__ void step(const TraceParams& p, const uint32_t* __restrict__ buf,
+                                       uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct, int& nt, uint32_t& nN) {
     ct.add(VF_CTR_STEPS);
     int Pn[3];
     float tn[3];
@@ -510,12 +530,18 @@ struct Lane {
     E.axis = a0;
     E.P = sel3(Pn, a0);
     E.t = sel3(tn, a0);
-    if (tmax_finite && cmp_es(r, E, r.tmax) >= 0) return IT_MISS;  // segment ends (reading A7)
+    if (tmax_finite && cmp_es(r, E, r.tmax) >= 0) {  // segment ends (reading A7)
+      nt = -1;
+      return;
+    }
     uint32_t h;
     if (S == (1 << a0)) {
       // common case: one axis steps into the cell adjacent to plane E.P
       const int nv = E.P - ((dneg >> a0) & 1);
-      if ((uint32_t)nv >= (uint32_t)sel3(p.dims, a0)) return IT_MISS;  // left the root box
+      if ((uint32_t)nv >= (uint32_t)sel3(p.dims, a0)) {  // left the root box
+        nt = -1;
+        return;
+      }
       h = 31u - __clz((uint32_t)(nv ^ sel3(V, a0)));
       V[0] = a0 == 0 ? nv : V[0];
       V[1] = a0 == 1 ? nv : V[1];
@@ -532,50 +558,26 @@ struct Lane {
         h = max(h, 31u - __clz((uint32_t)(nv ^ V[a])));
         V[a] = nv;
       }
-      if (out_of_box) return IT_MISS;  // left the root box
+      if (out_of_box) {  // left the root box
+        nt = -1;
+        return;
+      }
     }
-    if (lc) stale |= ~S & moving;
+    if (lc) {
+      stale |= ~S & moving;
+      stale_lc = max(stale_lc, lc);
+    }
     stale &= ~S;
     const int tau = (int)field4(p.tau_pack, h);
     if (tau < t) {
       ct.add(VF_CTR_POPS);
       // left the current node: pop (stack) or restart from the level root
-      if (!RESTART) {
-        set_tier(p, tau);
-        N = stk[tau];
-        hd = load_header<KINDS>(buf, kind, N, ct);
-      } else {
-        const int top = (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tau);
-        set_tier(p, top);
-        N = stk[top];
-        hd = load_header<KINDS>(buf, kind, N, ct);
-        while (t < tau) {  // re-descend through nodes that contain the current cell
-          const uint32_t lin = (((uint32_t)V[0] >> lc) & msk) + ((((uint32_t)V[1] >> lc) & msk) << sx) +
-                               ((((uint32_t)V[2] >> lc) & msk) << sxy);
-          const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
-          uint32_t child;
-          if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
-            child = hd.base + 2u * rank;
-          } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-#if VF_SVDAG_WIDE
-            const uint32_t i = hd.k + 1u + rank;
-            child = i < 8u ? sel8(hd.a, hd.b, i) : __ldg(buf + hd.base + 1u + rank);
-#else
-            child = __ldg(buf + hd.base + 1u + rank);
-#endif
-            ct.add(VF_CTR_SVDAG_PTRS);
-            ct.add(VF_CTR_FORMAT_BYTES, 4);
-          } else {
-            child = hd.base + 4u * rank;  // N^3 internal (t < tau <= last tier of the level)
-          }
-          set_tier(p, t + 1);
-          N = child;
-          hd = load_header<KINDS>(buf, kind, N, ct);
-          ct.add(VF_CTR_REDESCENTS);
-        }
-      }
+      // (restart: from the top of tau's level — the following iterations re-descend through the
+      //  nodes that contain the current cell as ordinary, always-occupied descents)
+      nt = RESTART ? (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tau) : tau;
+      nN = stk[nt];
+      if (RESTART) ct.add(VF_CTR_REDESCENTS, tau - nt);
     }
-    return IT_CONTINUE;
   }
 
   __device__ __forceinline__ int4 hit_record() const { return make_int4(V[0], V[1], V[2], __float_as_int(E.t)); }
