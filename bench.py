@@ -7,7 +7,7 @@ inputs.city), 1920x1080 aerial perspective rays, format R(4^3) G(7) (the paper's
 the one trace kernel); inputs are resident in HBM; L2 (126 MB) is flushed between timed steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config cfg4] [--format "R(4^3) G(7)"] [--restart] [--sweep]
+                  [--config cfg4] [--format "R(4^3) G(7)"] [--restart] [--no-sweep]
 
 Multi-GPU (torchrun, one rank per GPU): the volume is replicated, the frame's 16x16 screen tiles
 are interleaved across ranks (tile mod N), each rank traces its tiles, and the hit buffers are
@@ -37,9 +37,18 @@ CONFIGS = {
     "cfg4": ("city", "city", "R(4, 4, 4) G(7)", "2048^3 synthetic city blocks, 1920x1080 aerial rays"),
     "cfg5": ("sparse", "sparse", "R(4, 4, 4) G(8)", "4096^3 sparse shells, 3840x2160 rays"),
 }
+# per-config format sweeps: Mrays/s per hybrid format vs bytes/voxel
 SWEEP = {
-    "cfg4": ["R(4, 4, 4) G(7)", "R(3, 3, 3) G(8)", "G(11)", "S(11)", "R(6, 6, 6) G(5)", "R(4, 4, 4) S(7)",
-             "R(1, 1, 1) T(2, 5)", "T(2, 4) R(3, 3, 3)", "R(4, 4, 4) R(4, 4, 4) R(3, 3, 3)", "R(8, 8, 8) G(3)"],
+    "cfg1": ["R(6, 6, 6)", "R(3, 3, 3) R(3, 3, 3)", "G(6)", "S(6)", "T(2, 3)"],
+    "cfg2": ["S(8)", "G(8)", "G(5) R(3, 3, 3)", "T(2, 4)", "R(8, 8, 8)", "R(3, 3, 3) G(5)"],
+    "cfg3": ["T(2, 2) T(2, 1) R(4, 4, 4)", "T(2, 1) T(2, 2) R(4, 4, 4)", "S(5) R(5, 5, 5)", "G(10)",
+             "R(3, 3, 3) G(7)", "T(2, 5)", "S(10)"],
+    "cfg4": ["R(4, 4, 4) G(7)", "R(3, 3, 3) G(8)", "G(11)", "S(11)", "R(6, 6, 6) G(5)", "R(8, 8, 8) G(3)",
+             "R(4, 4, 4) S(7)", "R(6, 6, 6) S(5)", "S(3) G(8)", "S(5) G(6)", "S(7) G(4)", "R(4, 4, 4) R(3, 3, 3) G(4)",
+             "R(4, 4, 4) S(3) G(4)", "R(4, 4, 4) R(4, 4, 4) R(3, 3, 3)", "R(1, 1, 1) T(2, 5)", "T(2, 4) R(3, 3, 3)",
+             "T(2, 2) T(2, 2) R(3, 3, 3)", "T(2, 3) R(5, 5, 5)"],
+    "cfg5": ["R(4, 4, 4) G(8)", "R(3, 3, 3) G(9)", "G(12)", "T(2, 6)", "S(12)", "R(4, 4, 4) T(2, 4)",
+             "R(4, 4, 4) R(4, 4, 4) R(4, 4, 4)"],
 }
 L2_BYTES = 126 * 2**20
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -148,7 +157,7 @@ def cpu_baseline(vol_desc, rays, gpu_xyz, gpu_t, budget_s=12.0):
     return {"value": done / total_s / 1e6, "unit": "Mrays/s", "cores": cores, "kind": "oracle",
             "sample": f"{done} of {n} rays (evenly strided) of the same frame; exact int128 DDA over the "
                       f"procedural occupancy (vg_voxel per visited cell), OpenMP {cores} threads; {total_s:.2f} s",
-            "parity_checked": checked, "parity_mismatches": bad}
+            "parity_checked": checked, "parity_mismatches": bad}, idx, ref
 
 
 def run_ours(args):
@@ -275,10 +284,10 @@ def run_ours(args):
         # ---- CPU baseline (oracle) on a bounded sample + parity of the sample
         hits_np = hits.cpu().numpy()
         gxyz, gt = hits_np[:, :3], hits_np[:, 3].view(np.float32)
-        cpu = None
+        cpu, ref_idx, ref = None, None, None
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
         if not args.no_cpu_baseline and world == 1:
-            sys.path.insert(0, os.path.join(ROOT, "tests"))
-            cpu = cpu_baseline(vol, rays_all, gxyz, gt, budget_s=args.cpu_budget)
+            cpu, ref_idx, ref = cpu_baseline(vol, rays_all, gxyz, gt, budget_s=args.cpu_budget)
 
         hit_rate = float((gxyz[:, 0] >= 0).mean())
         bpv = stats["bytes_used"] / max(nonempty, 1)
@@ -302,8 +311,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "clocks": clk,
         }
-        if args.sweep and cfg in SWEEP:
-            result["sweep"] = sweep(cfg, vol, rays, hits, stream, flush, args)
+        if not args.no_sweep and world == 1 and cfg in SWEEP:
+            result["sweep"] = sweep(cfg, vol, rays, hits, stream, flush, args, ref_idx, ref)
     if world > 1:
         dist.destroy_process_group()
     return result
@@ -319,13 +328,23 @@ def algorithmic_bytes(handle, rays, restart, n):
     return {"bytes_per_launch": b, "bytes_per_ray": b / n, **c}
 
 
-def sweep(cfg, vol, rays, hits, stream, flush, args):
+def sweep(cfg, vol, rays, hits, stream, flush, args, ref_idx=None, ref=None):
+    """Every format of the config's sweep: Mrays/s (stack and restart), bytes/voxel (device and
+    paper layout), algorithmic bytes/ray from the counting kernel, the HBM roofline fraction, and
+    parity of the oracle-checked sample (the same rays the cpu_baseline leg traced)."""
     import torch
     import inputs
+    from parity import compare
     from paper_2410_14128_b200 import vf
     keys, rgba = inputs.voxels_device(vol)
     dims = inputs.dims_of(vol)
+    hbm = peaks().get("hbm_gbs")
+    try:
+        traffic = json.load(open(PROFILE_TRAFFIC))
+    except Exception:
+        traffic = {}
     out = []
+    n = rays.shape[0]
     for fmt in SWEEP[cfg]:
         try:
             h = vf.build((keys, rgba, dims), fmt)
@@ -334,10 +353,12 @@ def sweep(cfg, vol, rays, hits, stream, flush, args):
             continue
         st = h.stats()
         for restart in (False, True):
+            c = h.counters(rays, hits, restart=restart)
+            alg = 48 * n + c["format_bytes"]
             for _ in range(3):
                 h.trace(rays, hits, restart=restart)
             ms = []
-            for i in range(5):
+            for i in range(7):
                 flush.fill_(i)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
@@ -345,11 +366,24 @@ def sweep(cfg, vol, rays, hits, stream, flush, args):
                 b.record(stream)
                 torch.cuda.synchronize()
                 ms.append(a.elapsed_time(b))
-            out.append({"format": h.signature, "variant": "restart" if restart else "stack",
-                        "mrays_s": round(rays.shape[0] / (statistics.median(ms) / 1e3) / 1e6, 1),
-                        "bytes_per_voxel": round(st["bytes_used"] / st["nonempty_voxels"], 4),
-                        "paper_bytes_per_voxel": round(st["paper_layout_bytes"] / st["nonempty_voxels"], 4),
-                        "mib": round(st["bytes_used"] / 2**20, 1)})
+            t_ms = statistics.median(ms)
+            variant = "restart" if restart else "stack"
+            row = {"format": h.signature, "variant": variant, "mrays_s": round(n / (t_ms / 1e3) / 1e6, 1),
+                   "bytes_per_voxel": round(st["bytes_used"] / st["nonempty_voxels"], 4),
+                   "paper_bytes_per_voxel": round(st["paper_layout_bytes"] / st["nonempty_voxels"], 4),
+                   "mib": round(st["bytes_used"] / 2**20, 1), "alg_bytes_per_ray": round(alg / n, 1),
+                   "roofline_frac": round(alg / (t_ms / 1e3) / 1e9 / hbm, 5) if hbm else None,
+                   "cells_per_ray": round(c["cell_tests"] / n, 2), "descents_per_ray": round(c["descents"] / n, 2),
+                   "simt_bound": round(c["cell_tests"] / max(c["warp_max_tests"], 1), 3)}
+            key = f"{cfg}|{h.signature}|{variant}"
+            if key in traffic:
+                row["dram_bytes_per_ray"] = round(traffic[key]["dram_bytes_per_launch"] / n, 1)
+            if ref is not None:
+                o = hits.cpu().numpy()
+                nb, _ = compare(o[ref_idx, :3], o[ref_idx, 3].view(np.float32), ref)
+                row["parity_mismatches"] = nb
+                row["parity_checked"] = int(len(ref_idx))
+            out.append(row)
         h.close()
     return out
 
@@ -404,7 +438,7 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--format", default=None)
     ap.add_argument("--restart", action="store_true")
-    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the per-format sweep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
