@@ -184,11 +184,27 @@ vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hi
   }
   vf_ray* d_rays = (vf_ray*)h->stage;
   vf_hit* d_hits = (vf_hit*)((char*)h->stage + ((rb + 255) & ~(size_t)255));
-  VF_CUDA_TRY(cudaMemcpyAsync(d_rays, host_rays, rb, cudaMemcpyHostToDevice, s));
-  vf_status st = launch_trace(h, d_rays, n, d_hits, trace_flags, s);
-  if (st != VF_OK) return st;
-  VF_CUDA_TRY(cudaMemcpyAsync(host_hits, d_hits, hb, cudaMemcpyDeviceToHost, s));
-  VF_CUDA_TRY(cudaStreamSynchronize(s));
+  // Pipeline: the frame is cut into chunks that alternate over kPipe internal streams, so the
+  // host->device copy of chunk i+1, the trace of chunk i and the device->host copy of chunk i-1
+  // overlap (two copy engines + the SMs). Every chunk has its own staging region: no reuse hazard.
+  if (!h->pipe[0]) {
+    for (int i = 0; i < kPipe; ++i) VF_CUDA_TRY(cudaStreamCreateWithFlags(&h->pipe[i], cudaStreamNonBlocking));
+    VF_CUDA_TRY(cudaEventCreateWithFlags(&h->pipe_ev, cudaEventDisableTiming));
+  }
+  VF_CUDA_TRY(cudaEventRecord(h->pipe_ev, s));  // order after prior work on the caller's stream
+  const uint64_t chunks = n >= (1ull << 18) ? (n >> 17 < 16 ? n >> 17 : 16) : 1;
+  const uint64_t per = (n + chunks - 1) / chunks;
+  for (uint64_t c = 0; c < chunks; ++c) {
+    cudaStream_t cs = h->pipe[c % kPipe];
+    if (c < (uint64_t)kPipe) VF_CUDA_TRY(cudaStreamWaitEvent(cs, h->pipe_ev, 0));
+    const uint64_t b = c * per, m = (b + per <= n) ? per : n - b;
+    if (!m) break;
+    VF_CUDA_TRY(cudaMemcpyAsync(d_rays + b, host_rays + b, m * sizeof(vf_ray), cudaMemcpyHostToDevice, cs));
+    vf_status st = launch_trace(h, d_rays + b, m, d_hits + b, trace_flags, cs);
+    if (st != VF_OK) return st;
+    VF_CUDA_TRY(cudaMemcpyAsync(host_hits + b, d_hits + b, m * sizeof(vf_hit), cudaMemcpyDeviceToHost, cs));
+  }
+  for (int i = 0; i < kPipe; ++i) VF_CUDA_TRY(cudaStreamSynchronize(h->pipe[i]));
   return VF_OK;
 }
 
@@ -251,6 +267,9 @@ void vf_destroy(vf_handle* h) {
   if (h->buf) cudaFree(h->buf);
   if (h->stage) cudaFree(h->stage);
   if (h->work) cudaFree(h->work);
+  for (int i = 0; i < kPipe; ++i)
+    if (h->pipe[i]) cudaStreamDestroy(h->pipe[i]);
+  if (h->pipe_ev) cudaEventDestroy(h->pipe_ev);
   delete h;
 }
 

@@ -67,15 +67,18 @@ struct Handle {
   uint32_t* buf = nullptr;  // device words
   uint64_t n_words = 0;
   vf_stats stats{};
-  // staging for vf_trace_host
+  // staging and pipeline streams for vf_trace_host
   void* stage = nullptr;
   size_t stage_bytes = 0;
+  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t pipe_ev = nullptr;
   // persistent-trace work counters: kWorkSlots x {next ray, finished blocks}, self-resetting
   unsigned long long* work = nullptr;
   mutable std::atomic<uint32_t> work_slot{0};
 };
 
 constexpr uint32_t kWorkSlots = 64;
+constexpr int kPipe = 3;
 // internal trace flag (ablation / tests): persistent warps with dynamic ray refill
 constexpr uint32_t VF_TRACE_PERSISTENT_WARPS = 1u << 30;
 
