@@ -36,6 +36,8 @@ CONFIGS = {
     "cfg3": ("terrain", "terrain", "T(2, 2) T(2, 1) R(4, 4, 4)", "1024^3 noise terrain/caves, 1920x1080 rays"),
     "cfg4": ("city", "city", "R(4, 4, 4) G(7)", "2048^3 synthetic city blocks, 1920x1080 aerial rays"),
     "cfg5": ("sparse", "sparse", "R(4, 4, 4) G(8)", "4096^3 sparse shells, 3840x2160 rays"),
+    # the paper's 512^3 Table 2 rows (21-40) on a 512^3 city (not a BASELINE config)
+    "t512": ("city512", "city512", "R(4, 4, 4) G(5)", "512^3 synthetic city blocks, 1024x1024 rays (Table 2 rows 21-40)"),
 }
 # per-config format sweeps: Mrays/s per hybrid format vs bytes/voxel
 SWEEP = {
@@ -50,6 +52,12 @@ SWEEP = {
     "cfg5": ["R(4, 4, 4) G(8)", "R(3, 3, 3) G(9)", "G(12)", "T(2, 6)", "S(12)", "R(4, 4, 4) T(2, 4)",
              "R(4, 4, 4) R(4, 4, 4) R(4, 4, 4)"],
 }
+# PAPER.md Table 2 (tests/golden/table2_formats.txt): rows 1-20 on cfg4, rows 21-40 on t512
+_T2 = [l.strip().split(" ", 2) for l in open(os.path.join(ROOT, "tests", "golden", "table2_formats.txt"))
+       if l.strip() and not l.startswith("#")]
+SWEEP["cfg4"] = SWEEP["cfg4"] + [sig for _, res, sig in _T2 if res == "2048" and
+                                 "D(" in sig]  # the DF rows (the others are already in the list)
+SWEEP["t512"] = [sig for _, res, sig in _T2 if res == "512"]
 L2_BYTES = 126 * 2**20
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
@@ -66,7 +74,7 @@ def dist_env():
 def make_volume(name):
     import inputs
     return {"sphere": inputs.sphere, "menger": inputs.menger, "terrain": inputs.terrain, "city": inputs.city,
-            "sparse": inputs.sparse}[name]()
+            "sparse": inputs.sparse, "city512": lambda: inputs.city(512)}[name]()
 
 
 def make_rays(cfg):

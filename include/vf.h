@@ -45,7 +45,7 @@ typedef enum {
   VF_ERR_PARSE = 2,       /* signature syntax; message gives the character position */
   VF_ERR_FORMAT = 3,      /* non-cubic or non-power-of-two non-first level,
                              depth 0, resolution != volume dims, more than VF_MAX_TIERS tiers */
-  VF_ERR_UNSUPPORTED = 4, /* valid paper format this build does not implement (DF, D(...)) */
+  VF_ERR_UNSUPPORTED = 4, /* valid format this build does not implement */
   VF_ERR_OVERFLOW = 5,    /* a stored offset would reach 2^32 words (PAPER.md:86, 16 GiB) */
   VF_ERR_OOM = 6,         /* device allocation failed */
   VF_ERR_CUDA = 7         /* CUDA runtime / launch error */
@@ -64,8 +64,9 @@ VF_API int vf_abi_version(void);
  *   VF_SVDAG G(L)    : de-duplicated octree of depth L, 1..9-word nodes
  *   VF_NTREE T(n,d)  : N^3-tree, N = 2^n, depth d, 16-B nodes with a 64-bit occupancy mask
  *                      (generalisation of SVO; layout is ours)
- *   VF_DF    D(W,H,D,M): distance field — parsed, not implemented
- *                      (VF_ERR_UNSUPPORTED), SURVEY §8(f) NEXT item 1.
+ *   VF_DF    D(W,H,D,M): Raw grid of {TermInt, L1 distance to the nearest non-empty cell,
+ *                      capped at M} pairs; traversal skips occupancy
+ *                      tests within the distance.
  * Every level but the first must be cubic with power-of-two extent. */
 enum { VF_RAW = 0, VF_SVO = 1, VF_SVDAG = 2, VF_NTREE = 3, VF_DF = 4 };
 
@@ -82,8 +83,8 @@ typedef struct {
 #define VF_MAX_TIERS 16 /* a tier = one node level: Raw 1, S(L)/G(L) L, T(n,d) d */
 
 /* Parse a signature: "R(3,3,3) G(8)", Table-2 sugar "R(3^3) G(8)" / "R(3³) G(8)" (PAPER.md
- * Table 2, :303-322), "S(11)", "T(2,2) T(2,1) R(4^3)", "D(4^3, 6) G(5)" (parsed, then
- * unsupported at build). Whitespace-separated levels; whitespace inside parentheses allowed.
+ * Table 2, :303-322), "S(11)", "T(2,2) T(2,1) R(4^3)", "D(4^3, 6) G(5)". Whitespace-separated
+ * levels; whitespace inside parentheses allowed.
  * out: caller array of capacity cap; *n_out = number of levels. VF_ERR_PARSE on syntax. */
 VF_API vf_status vf_parse_format(const char* sig, vf_level* out, uint32_t cap, uint32_t* n_out);
 
@@ -181,7 +182,7 @@ enum {
   VF_CTR_REDESCENTS,    /* restart variant: levels re-descended from the sub-volume root */
   VF_CTR_LOCATES,       /* certified sub-cell locates (entry + descents at stale events) */
   VF_CTR_NEAR_TIES,     /* DDA steps whose argmin needed the pairwise exact path */
-  VF_CTR_RAW_CELLS,     /* Raw cells read (4 B) */
+  VF_CTR_RAW_CELLS,     /* Raw cells read (4 B; DF cells 8 B) */
   VF_CTR_SVO_NODES,     /* SVO node headers read (8 B) */
   VF_CTR_SVDAG_NODES,   /* SVDAG masks read (4 B) */
   VF_CTR_SVDAG_PTRS,    /* SVDAG child pointers read (4 B) */
@@ -190,6 +191,7 @@ enum {
   VF_CTR_FORMAT_BYTES,  /* sum of the above in bytes */
   VF_CTR_EXACT_CALLS,   /* exact fallbacks (device-global counter) */
   VF_CTR_WARP_MAX_TESTS, /* sum over warps of 32 x (max cell tests of a lane): SIMT bound */
+  VF_CTR_DF_SKIPS,      /* DF cells passed without a memory access (distance budget) */
   VF_NCOUNTERS
 };
 

@@ -202,6 +202,9 @@ CAMERAS = {
                  target=(1024.0, 200.0, 1024.0)),
     "city_street": dict(width=1920, height=1080, fov_deg=60.0, eye=(16.5, 40.25, 8.75),
                         target=(1024.0, 120.0, 1024.0)),
+    # Table 2 512^3 rows: 512^3 city, 1024^2 aerial
+    "city512": dict(width=1024, height=1024, fov_deg=60.0, eye=(-50.5, 400.25, -75.75),
+                    target=(256.0, 50.0, 256.0)),
     # cfg5: 4096^3 sparse, 3840x2160, fov 75, outside one corner
     "sparse": dict(width=3840, height=2160, fov_deg=75.0, eye=(-300.5, -250.25, -350.75),
                    target=(2048.0, 2048.0, 2048.0)),

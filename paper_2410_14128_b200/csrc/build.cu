@@ -147,15 +147,59 @@ __device__ inline void local_xyz(uint64_t ck, bool root, uint32_t lf, uint32_t* 
 }
 
 // ---------------------------------------------------------------- RAW tier
+// cw = words per cell: 1 (Raw) or 2 (DF: {TermInt, L1 distance})
 __global__ void k_raw_scatter(const uint64_t* ck, const uint4* cr, const uint32_t* node_of, uint64_t n, bool root,
-                              uint32_t lf, uint32_t lfx, uint32_t lfy, uint64_t F, uint32_t* arr) {
+                              uint32_t lf, uint32_t lfx, uint32_t lfy, uint64_t F, uint32_t cw, uint32_t* arr) {
   GRID_STRIDE(i, n) {
     uint32_t lx, ly, lz;
     local_xyz(ck[i], root, lf, &lx, &ly, &lz);
     uint64_t li = root ? ((uint64_t)lx + ((uint64_t)ly << lfx) + ((uint64_t)lz << (lfx + lfy)))
                        : ((uint64_t)lx + ((uint64_t)ly << lf) + ((uint64_t)lz << (2 * lf)));
-    arr[(uint64_t)node_of[i] * F + li] = cr[i].x;
+    arr[((uint64_t)node_of[i] * F + li) * cw] = cr[i].x;
   }
+}
+
+// DF: L1 distance of every cell to the nearest non-empty cell of its grid ("the L1
+// norm distance to the nearest non-empty voxel"; construction PAPER.md:197), capped at M. The
+// L1 distance transform is separable: exact two-pass (forward / backward) 1-D min-plus sweeps
+// along x, then y, then z. One thread per line of one node.
+constexpr uint32_t kDfInf = 1u << 24;
+
+__global__ void k_df_init(uint32_t* arr, uint64_t cells) {
+  GRID_STRIDE(i, cells) { arr[2 * i + 1] = arr[2 * i] ? 0u : kDfInf; }
+}
+
+__global__ void k_df_pass(uint32_t* arr, uint64_t M, uint32_t lfx, uint32_t lfy, uint32_t lfz, int axis) {
+  const uint32_t l[3] = {lfx, lfy, lfz};
+  const uint32_t la = l[axis], lo0 = l[(axis + 1) % 3], lo1 = l[(axis + 2) % 3];
+  const uint64_t F = 1ull << (lfx + lfy + lfz);
+  const uint64_t lines = M << (lo0 + lo1);
+  const uint64_t sh[3] = {0, lfx, (uint64_t)lfx + lfy};  // cell index = x + (y << lfx) + (z << lfx+lfy)
+  GRID_STRIDE(j, lines) {
+    const uint64_t m = j >> (lo0 + lo1);
+    const uint64_t u = j & ((1ull << lo0) - 1), v = (j >> lo0) & ((1ull << lo1) - 1);
+    const uint64_t base = m * F + (u << sh[(axis + 1) % 3]) + (v << sh[(axis + 2) % 3]);
+    const uint64_t step = 1ull << sh[axis];
+    const uint64_t len = 1ull << la;
+    uint32_t prev = kDfInf;
+    for (uint64_t k = 0; k < len; ++k) {
+      uint32_t* d = arr + 2 * (base + k * step) + 1;
+      const uint32_t x = min(*d, prev + 1);
+      *d = x;
+      prev = x;
+    }
+    prev = kDfInf;
+    for (uint64_t k = len; k-- > 0;) {
+      uint32_t* d = arr + 2 * (base + k * step) + 1;
+      const uint32_t x = min(*d, prev + 1);
+      *d = x;
+      prev = x;
+    }
+  }
+}
+
+__global__ void k_df_cap(uint32_t* arr, uint64_t cells, uint32_t dmax) {
+  GRID_STRIDE(i, cells) { arr[2 * i + 1] = min(arr[2 * i + 1], dmax); }
 }
 
 __global__ void k_raw_refs(uint64_t M, uint64_t base, uint64_t F, uint4* nr) {
@@ -466,11 +510,21 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
 
       if (T.kind == K_RAW) {
         const uint64_t F = 1ull << (T.lf[0] + T.lf[1] + T.lf[2]);
-        words = pwords = M * F;
+        const uint32_t cw = T.df ? 2u : 1u;
+        words = pwords = M * F * cw;
         arr.assign(words, 0u);
         k_raw_scatter<<<grid_for(n), kThreads, 0, s>>>(raw(ck), raw(cr), raw(node_of), n, is_root, lf, T.lf[0],
-                                                        T.lf[1], F, raw(arr));
-        k_raw_refs<<<grid_for(M), kThreads, 0, s>>>(M, base, F, raw(nr));
+                                                        T.lf[1], F, cw, raw(arr));
+        if (T.df) {
+          const uint64_t cells = M * F;
+          k_df_init<<<grid_for(cells), kThreads, 0, s>>>(raw(arr), cells);
+          for (int a = 0; a < 3; ++a) {
+            const uint64_t lines = cells >> T.lf[a];
+            k_df_pass<<<grid_for(lines), kThreads, 0, s>>>(raw(arr), M, T.lf[0], T.lf[1], T.lf[2], a);
+          }
+          k_df_cap<<<grid_for(cells), kThreads, 0, s>>>(raw(arr), cells, T.df_max);
+        }
+        k_raw_refs<<<grid_for(M), kThreads, 0, s>>>(M, base, F * cw, raw(nr));
       } else if (T.kind == K_SVO || T.kind == K_NTREE) {
         thrust::device_vector<uint64_t> size(M), paper(M), off(M);
         k_inline_sizes<<<grid_for(M), kThreads, 0, s>>>(raw(node_start), M, n, T.kind, T.top, T.last, raw(size),

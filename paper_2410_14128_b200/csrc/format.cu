@@ -227,14 +227,27 @@ vf_status expand_format(const vf_level* levels, uint32_t n, Format* f) {
         kind = K_NTREE;
         break;
       case VF_DF:
-        if (l > 0 && (L.log2_extent[0] != L.log2_extent[1] || L.log2_extent[1] != L.log2_extent[2])) {
-          set_error("level %u D(...) is not cubic (PAPER.md:267)", l + 1);
+        // D(W,H,D,M): a Raw grid whose cells also store the L1
+        // distance to the nearest non-empty cell, capped at M; traversed as a Raw tier that
+        // skips occupancy tests while the distance budget lasts
+        for (int a = 0; a < 3; ++a) lf[a] = L.log2_extent[a];
+        if (l > 0 && (lf[0] != lf[1] || lf[1] != lf[2])) {
+          set_error("level %u D(%u,%u,%u,%u) is not cubic: every level but the first must be cubic with "
+                    "power-of-two extent (PAPER.md:267)",
+                    l + 1, lf[0], lf[1], lf[2], L.df_max);
           return VF_ERR_FORMAT;
         }
-        set_error("level %u: the DF base format D(W,H,D,M) (PAPER.md:75) is not implemented in this build "
-                  "(SURVEY.md §8(f) NEXT)",
-                  l + 1);
-        return VF_ERR_UNSUPPORTED;
+        for (int a = 0; a < 3; ++a)
+          if (lf[a] > 12) {
+            set_error("level %u: DF extent 2^%u exceeds 4096", l + 1, lf[a]);
+            return VF_ERR_FORMAT;
+          }
+        if (L.df_max < 1) {
+          set_error("level %u: D(...,M) needs M >= 1", l + 1);
+          return VF_ERR_FORMAT;
+        }
+        kind = K_RAW;
+        break;
       default:
         set_error("level %u: unknown kind %u", l + 1, L.kind);
         return VF_ERR_FORMAT;
@@ -251,6 +264,8 @@ vf_status expand_format(const vf_level* levels, uint32_t n, Format* f) {
       T.depth = r;
       T.top = r == 0;
       T.last = r + 1 == reps;
+      T.df = L.kind == VF_DF;
+      T.df_max = L.kind == VF_DF ? L.df_max : 0;
       T.lc = 0;
     }
   }
@@ -278,6 +293,7 @@ TraceParams make_trace_params(const Format& f, uint32_t root) {
     p.lf_pack |= (uint64_t)(T.lf[0] & 15) << (4 * t);
     p.kind_pack |= T.kind << (2 * t);
     if (T.top) p.top_mask |= 1u << t;
+    if (T.df) p.df_mask |= 1u << t;
     if (T.last) p.last_mask |= 1u << t;
     uint32_t top = t - T.depth;
     if (t < 8)
@@ -351,7 +367,6 @@ vf_status vf_format_to_string(const vf_level* levels, uint32_t n, char* buf, siz
 vf_status vf_format_resolution(const vf_level* levels, uint32_t n, uint32_t dims[3]) {
   clear_error();
   Format f;
-  // DF levels have a resolution even though this build cannot construct them
   vf_level tmp[VF_MAX_LEVELS];
   if (n > VF_MAX_LEVELS || !levels || !dims) {
     set_error("vf_format_resolution: bad arguments");
@@ -359,7 +374,6 @@ vf_status vf_format_resolution(const vf_level* levels, uint32_t n, uint32_t dims
   }
   for (uint32_t l = 0; l < n; ++l) {
     tmp[l] = levels[l];
-    if (tmp[l].kind == VF_DF) tmp[l].kind = VF_RAW;
   }
   vf_status st = expand_format(tmp, n, &f);
   if (st != VF_OK) return st;

@@ -349,7 +349,8 @@ struct Lane {
   bool tmax_finite;
   // cached parameters of tier t
   uint32_t lc, msk, sx, sxy;
-  bool last, finest;
+  bool last, finest, df;
+  int budget;  // DF tier: remaining L1 distance within which every cell is known empty
   // (the per-tier node stack lives outside the struct so that the struct itself can stay in
   //  registers: an indexed member would force the whole object into local memory)
 
@@ -363,6 +364,8 @@ struct Lane {
     sxy = nt == 0 ? p.lf0[0] + p.lf0[1] : 2 * lf;
     last = (p.last_mask >> nt) & 1u;
     finest = nt == (int)p.n_tiers - 1;
+    df = (p.df_mask >> nt) & 1u;
+    budget = 0;
   }
 
   // ---- root function: word 0, root-box test, exact entry cell ---------------
@@ -437,10 +440,24 @@ struct Lane {
       if (has_kind<KINDS>(K_RAW) && kind == K_RAW) {
         // 64-bit index: a single-level R(11^3) grid has 2^33 cells (reading A15)
         const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
-        child = __ldg(buf + (size_t)N + lin);
-        occ = child != 0u;
-        ct.add(VF_CTR_RAW_CELLS);
-        ct.add(VF_CTR_FORMAT_BYTES, 4);
+        if (!df) {
+          child = __ldg(buf + (size_t)N + lin);
+          occ = child != 0u;
+          ct.add(VF_CTR_RAW_CELLS);
+          ct.add(VF_CTR_FORMAT_BYTES, 4);
+        } else if (budget > 0) {
+          // DF: within L1 distance `budget` of a cell whose nearest non-empty cell is that far
+          // away, so empty without a memory access ("how many voxels can be
+          // marched through before checking occupancy")
+          ct.add(VF_CTR_DF_SKIPS);
+        } else {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(buf + (size_t)N + 2 * lin));
+          child = v.x;
+          occ = child != 0u;
+          budget = (int)v.y;
+          ct.add(VF_CTR_RAW_CELLS);
+          ct.add(VF_CTR_FORMAT_BYTES, 8);
+        }
       } else {
         const uint32_t lin = lx + (ly << sx) + (lz << sxy);
         occ = (hd.mask >> lin) & 1u;
@@ -568,6 +585,7 @@ struct Lane {
       stale_lc = max(stale_lc, lc);
     }
     stale &= ~S;
+    budget -= __popc(S);  // L1 distance moved (DF tiers only use it)
     const int tau = (int)field4(p.tau_pack, h);
     if (tau < t) {
       ct.add(VF_CTR_POPS);
@@ -699,7 +717,7 @@ __global__ void query_kernel(const TraceParams p, const uint32_t* __restrict__ b
         const bool last = (p.last_mask >> t) & 1u;
         uint32_t word;
         if (kind == K_RAW) {
-          word = buf[(size_t)N + lin];
+          word = buf[(size_t)N + (size_t)lin * (((p.df_mask >> t) & 1u) ? 2u : 1u)];
         } else {
           uint64_t mask;
           uint32_t base;

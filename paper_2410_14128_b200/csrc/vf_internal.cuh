@@ -30,6 +30,8 @@ struct Tier {
   uint32_t depth;  // depth within its level (0 = level top)
   bool top;        // first tier of its level (its node is the level's sub-volume root)
   bool last;       // last tier of its level (its cells are terminating integers)
+  bool df;         // K_RAW tier of a DF level D(W,H,D,M): cells are {TermInt, L1 distance} pairs
+  uint32_t df_max; // DF: maximum stored L1 distance M
 };
 
 struct Format {
@@ -52,6 +54,7 @@ struct TraceParams {
   uint32_t top_mask;    // bit t: tier t is its level's top
   uint32_t last_mask;   // bit t: tier t is its level's last tier
   uint32_t refill;      // persistent trace: refill a warp when >= refill lanes are idle
+  uint32_t df_mask;     // bit t: tier t is a DF grid (2-word cells {TermInt, L1 distance})
   uint32_t lf0[3];      // tier-0 fan-out per axis (log2)
   int32_t dims[3];      // resolution per axis
   uint32_t n_tiers;

@@ -54,6 +54,7 @@ SMALL_FORMATS_16 = [
     "S(2) R(2, 2, 2)", "T(2, 1) R(2^3)", "T(2, 1) T(1, 1) R(1^3)", "R(1, 1, 1) T(2, 1) S(1)",
     "R(1^3) S(1) G(1) T(1, 1)", "G(1) T(2, 1) R(1^3)", "R(2^3) R(2^3)", "S(1) S(1) S(1) S(1)",
     "G(3) G(1)", "T(2, 1) T(2, 1)",
+    "D(4, 4, 4, 3)", "D(2^3, 2) G(2)", "R(1^3) D(3^3, 6)", "D(2^3, 6) D(2^3, 1)", "S(2) D(2^3, 4)",
 ]
 
 
@@ -74,7 +75,7 @@ def test_small_formats_vs_oracle(fmt, p):
 
 @pytest.mark.parametrize("fmt,dims", [
     ("R(2, 1, 3) G(2)", (16, 8, 32)), ("R(0, 2, 1) S(3)", (8, 32, 16)), ("R(3, 0, 1) T(2, 1) R(1^3)", (64, 8, 16)),
-    ("R(1, 2, 0) R(2^3)", (8, 16, 4)),
+    ("R(1, 2, 0) R(2^3)", (8, 16, 4)), ("D(1, 2, 0, 3) R(2^3)", (8, 16, 4)), ("D(3, 1, 2, 6) G(2)", (32, 8, 16)),
 ])
 def test_noncubic_first_level(fmt, dims):
     vf = _vf()
@@ -88,7 +89,8 @@ def test_noncubic_first_level(fmt, dims):
 
 
 # ---------------------------------------------------------------- cfg2: 256^3 Menger
-CFG2_FORMATS = ["S(8)", "G(8)", "G(5) R(3, 3, 3)", "T(2, 4)", "R(8, 8, 8)", "R(3^3) G(5)"]
+CFG2_FORMATS = ["S(8)", "G(8)", "G(5) R(3, 3, 3)", "T(2, 4)", "R(8, 8, 8)", "R(3^3) G(5)", "D(4^3, 6) G(4)",
+                "D(8^3, 6)", "D(3^3, 6) D(3^3, 6) R(2^3)"]
 
 
 @pytest.mark.parametrize("fmt", CFG2_FORMATS)
@@ -177,8 +179,8 @@ def test_format_errors():
         vf.build(v, "R(2, 2, 2) R(1, 2, 1)")
     assert e.value.status == vf.VF_ERR_FORMAT
     with pytest.raises(vf.VfError) as e:
-        vf.build(v, "D(2^3, 6) G(2)")
-    assert e.value.status == vf.VF_ERR_UNSUPPORTED
+        vf.build(v, "R(1, 1, 1) D(1, 2, 1, 6) G(1)")
+    assert e.value.status == vf.VF_ERR_FORMAT
     with pytest.raises(vf.VfError) as e:
         vf.build(v, "G(5)")
     assert e.value.status == vf.VF_ERR_FORMAT
@@ -264,3 +266,81 @@ def test_full_size_sampled(cfg, fmt):
             xyz, t = np.concatenate([xyz, x2]), np.concatenate([t, t2])
         assert_parity(xyz, t, ref, f"{cfg} {fmt} restart={restart}")
     h.close()
+
+
+# ---------------------------------------------------------------- DF distance field
+@pytest.mark.parametrize("fmt,M", [("D(4, 4, 4, 5)", 5), ("R(1^3) D(3^3, 6)", 6), ("D(4, 3, 4, 2)", 2)])
+def test_df_distances_are_exact_l1(fmt, M):
+    """Every DF cell stores min(M, L1 distance to the nearest non-empty cell of its grid)
+    (PAPER.md:59, :100-105): checked against a brute-force L1 distance transform."""
+    import torch
+    vf = _vf()
+    L = vf.parse_format(fmt)
+    dims = vf.format_resolution(L)
+    d = inputs.random_occupancy(dims, 0.02, 31)
+    dense = inputs.dense_host(d)
+    h = vf.build(torch.from_numpy(dense.view(np.int32)).cuda(), fmt)
+    words = h.buffer_words()
+    Rx, Ry, Rz = dims
+    # locate the DF grids: single level -> one grid at word[0]; R(1^3) D(..) -> 8 sub-grid pointers
+    if fmt.startswith("D"):
+        grids = [(words[0], (0, 0, 0), (Rx, Ry, Rz))]
+    else:
+        top = words[0]
+        e = Rx // 2
+        grids = []
+        for z in range(2):
+            for y in range(2):
+                for x in range(2):
+                    ptr = words[top + x + 2 * (y + 2 * z)]
+                    if ptr:
+                        grids.append((ptr, (x * e, y * e, z * e), (e, e, e)))
+    assert grids
+    for ptr, o, ext in grids:
+        sub = dense[o[2]:o[2] + ext[2], o[1]:o[1] + ext[1], o[0]:o[0] + ext[0]] != 0
+        occ = np.argwhere(sub)  # (z, y, x)
+        zz, yy, xx = np.meshgrid(np.arange(ext[2]), np.arange(ext[1]), np.arange(ext[0]), indexing="ij")
+        cells = np.stack([zz.ravel(), yy.ravel(), xx.ravel()], 1)
+        dist = np.abs(cells[:, None, :] - occ[None, :, :]).sum(-1).min(1)
+        expect = np.minimum(dist, M)
+        n = ext[0] * ext[1] * ext[2]
+        got = words[ptr:ptr + 2 * n].reshape(n, 2)
+        np.testing.assert_array_equal(got[:, 1], expect, err_msg=fmt)
+        np.testing.assert_array_equal(got[:, 0], dense[o[2]:o[2] + ext[2], o[1]:o[1] + ext[1],
+                                                        o[0]:o[0] + ext[0]].ravel())
+
+
+# ---------------------------------------------------------------- the paper's Table 2 (all 40 formats)
+def _table2():
+    import os
+    rows = []
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "table2_formats.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        label, res, sig = line.strip().split(" ", 2)
+        rows.append((int(label), int(res), sig))
+    return rows
+
+
+@pytest.mark.parametrize("res", [512, 2048])
+def test_table2_formats_parity(res):
+    """Every format of PAPER.md Table 2 (rows 1-20 at 2048^3 on the cfg4 city, rows 21-40 at
+    512^3 on the t512 city), stack and restart, against the oracle on a strided frame sample."""
+    import torch
+    import bench
+    vf = _vf()
+    cfg = "cfg4" if res == 2048 else "t512"
+    vol = bench.make_volume(bench.CONFIGS[cfg][0])
+    keys, rgba = inputs.voxels_device(vol)
+    rays, _ = bench.make_rays(cfg)
+    idx = np.arange(0, len(rays), 97)
+    ref = oracle.Grid.procedural(vol).trace(rays[idx])
+    rt = torch.from_numpy(rays).cuda()
+    for label, r, sig in _table2():
+        if r != res:
+            continue
+        h = vf.build((keys, rgba, inputs.dims_of(vol)), sig)
+        for restart in (False, True):
+            out = h.trace(rt, restart=restart).cpu().numpy()
+            assert_parity(out[idx, :3], out[idx, 3].view(np.float32), ref, f"Table 2 row {label} {sig} restart={restart}")
+        h.close()
