@@ -36,6 +36,8 @@ CONFIGS = {
     "cfg3": ("terrain", "terrain", "T(2, 2) T(2, 1) R(4, 4, 4)", "1024^3 noise terrain/caves, 1920x1080 rays"),
     "cfg4": ("city", "city", "R(4, 4, 4) G(7)", "2048^3 synthetic city blocks, 1920x1080 aerial rays"),
     "cfg5": ("sparse", "sparse", "R(4, 4, 4) G(8)", "4096^3 sparse shells, 3840x2160 rays"),
+    # incoherent secondary-style rays through the cfg4 city (not a BASELINE config)
+    "cfg4i": ("city", "incoherent", "R(4, 4, 4) G(7)", "2048^3 city, 2073600 incoherent rays (uniform origins in the lower city, random directions, tmax 256)"),
     # the paper's 512^3 Table 2 rows (21-40) on a 512^3 city (not a BASELINE config)
     "t512": ("city512", "city512", "R(4, 4, 4) G(5)", "512^3 synthetic city blocks, 1024x1024 rays (Table 2 rows 21-40)"),
 }
@@ -58,6 +60,8 @@ _T2 = [l.strip().split(" ", 2) for l in open(os.path.join(ROOT, "tests", "golden
 SWEEP["cfg4"] = SWEEP["cfg4"] + [sig for _, res, sig in _T2 if res == "2048" and
                                  "D(" in sig]  # the DF rows (the others are already in the list)
 SWEEP["t512"] = [sig for _, res, sig in _T2 if res == "512"]
+SWEEP["cfg4i"] = ["R(4, 4, 4) G(7)", "R(3, 3, 3) G(8)", "G(11)", "S(11)", "R(6, 6, 6) G(5)", "R(1, 1, 1) T(2, 5)",
+                  "D(6, 6, 6, 6) G(5)", "R(8, 8, 8) G(3)"]
 L2_BYTES = 126 * 2**20
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
@@ -82,6 +86,9 @@ def make_rays(cfg):
     vol, cam, _, _ = CONFIGS[cfg]
     if cam is None:
         return R.ortho(256, 256, 0.25, -1.0)
+    if cam == "incoherent":
+        n = 1920 * 1080
+        return R.incoherent(n, (0, 16, 0), (2048, 400, 2048), 0x5EC0, tmax=256.0), np.arange(n)
     return R.camera(cam)
 
 
@@ -199,7 +206,7 @@ def run_ours(args):
     from inputs.rays import CAMERAS
     from paper_2410_14128_b200 import shard
     cam = CONFIGS[cfg][1]
-    width = 256 if cam is None else CAMERAS[cam]["width"]
+    width = 256 if cam is None else (1920 if cam == "incoherent" else CAMERAS[cam]["width"])
     own = shard.shard(perm, width, rank, world)
     rays = torch.from_numpy(np.ascontiguousarray(rays_all[own])).to(dev)
     n_local = rays.shape[0]
@@ -283,6 +290,23 @@ def run_ours(args):
         except Exception:
             pass
         achieved = alg["bytes_per_launch"] / (kmean / 1e3) / 1e9
+        # issue roofline: warp instructions per launch (ncu smsp__inst_executed.sum, same kernel
+        # and workload) / measured kernel time vs 148 SMs x 4 schedulers x 1 warp-inst / cycle
+        issue = None
+        try:
+            tj = json.load(open(PROFILE_TRAFFIC))
+            ent = tj.get(f"{cfg}|{handle.signature}|{'restart' if args.restart else 'stack'}", {})
+            wi = ent.get("warp_inst_per_launch")
+            if wi:
+                sm_mhz = (clk or {}).get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+                peak_i = 148 * 4 * sm_mhz * 1e6
+                ach_i = wi / (kmean / 1e3)
+                issue = {"bound": "issue", "achieved": round(ach_i / 1e9, 2), "peak": round(peak_i / 1e9, 2),
+                         "unit": "Gwarp-inst/s", "frac": round(ach_i / peak_i, 4),
+                         "warp_inst_per_ray": round(wi / n_local, 1),
+                         "simt_threads_per_inst": round(ent.get("thread_inst_per_launch", 0) / wi, 2)}
+        except Exception:
+            pass
         roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 5) if hbm else None, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if hbm else "missing",
@@ -316,6 +340,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": n_local * 16},
             "gpu_launches": args.steps,
             "roofline": roof,
+            "issue_roofline": issue,
             "cpu_baseline": cpu,
             "clocks": clk,
         }
@@ -360,6 +385,11 @@ def sweep(cfg, vol, rays, hits, stream, flush, args, ref_idx=None, ref=None):
             out.append({"format": fmt, "error": str(e)})
             continue
         st = h.stats()
+        no_wld = None
+        if "G(" in h.signature:  # whole-level de-dup ablation: bytes only
+            h2 = vf.build((keys, rgba, dims), fmt, flags=0)
+            no_wld = h2.stats()["bytes_used"]
+            h2.close()
         for restart in (False, True):
             c = h.counters(rays, hits, restart=restart)
             alg = 48 * n + c["format_bytes"]
@@ -380,6 +410,7 @@ def sweep(cfg, vol, rays, hits, stream, flush, args, ref_idx=None, ref=None):
                    "bytes_per_voxel": round(st["bytes_used"] / st["nonempty_voxels"], 4),
                    "paper_bytes_per_voxel": round(st["paper_layout_bytes"] / st["nonempty_voxels"], 4),
                    "mib": round(st["bytes_used"] / 2**20, 1), "alg_bytes_per_ray": round(alg / n, 1),
+                   "wld_reduction": round(no_wld / st["bytes_used"], 3) if no_wld else None,
                    "roofline_frac": round(alg / (t_ms / 1e3) / 1e9 / hbm, 5) if hbm else None,
                    "cells_per_ray": round(c["cell_tests"] / n, 2), "descents_per_ray": round(c["descents"] / n, 2),
                    "simt_bound": round(c["cell_tests"] / max(c["warp_max_tests"], 1), 3)}

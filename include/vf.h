@@ -156,6 +156,22 @@ enum {
 VF_API vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t trace_flags,
                    void* cuda_stream);
 
+/* Closest-hit payload (the paper's closest-hit shader):
+ * rgba = the hit voxel's stored word (its RGBA; 0 on a miss); normal = the entry
+ * face: normal[a] = -sign(d_a) for the lowest axis a whose voxel-slab entry plane is crossed
+ * exactly at the hit t (edge / corner entries tie several axes), all 0 when the segment starts
+ * inside the hit voxel (t = tmin) and on a miss. */
+typedef struct {
+  uint32_t rgba;
+  int8_t normal[3];
+  int8_t reserved;
+} vf_payload; /* 8 B */
+
+/* vf_trace plus an optional payload output (device array of n vf_payload, 8-B aligned; NULL
+ * = none). Same kernel; the payload costs one extra load per hit ray. */
+VF_API vf_status vf_trace_ex(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, vf_payload* payload,
+                             uint32_t trace_flags, void* cuda_stream);
+
 /* End-to-end variant with HOST buffers: copies rays host->device, traces, copies hits
  * device->host and returns when the hits are on the host. Large frames are cut into chunks
  * pipelined over the handle's internal streams (copy-in of chunk i+1, trace of chunk i and

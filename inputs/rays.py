@@ -217,3 +217,17 @@ def camera(name: str, scale: int = 1):
     c["width"] //= scale
     c["height"] //= scale
     return perspective(**c)
+
+
+def incoherent(n: int, lo, hi, seed: int, tmax: float = np.inf):
+    """Incoherent secondary-style rays (the regime where memory binds):
+    origins uniform in the box [lo, hi), directions uniform on the sphere, segment [0, tmax).
+    Adjacent rays share nothing, so a warp's 32 rays touch 32 unrelated paths."""
+    rng = np.random.Generator(np.random.MT19937(seed))
+    lo = np.asarray(lo, dtype=np.float64)
+    hi = np.asarray(hi, dtype=np.float64)
+    o = lo + rng.random((n, 3)) * (hi - lo)
+    o = np.round(o * 64) / 64 + 1.0 / 128  # dyadic, never exactly on a plane
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return pack(o, d, 0.0, tmax)

@@ -4,7 +4,7 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl refe
 legs may import this package. The product path (paper_2410_14128_b200/) never imports it
 and shares no code with it (the one shared module is ``inputs``, the seeded input
 generators). See oracle/oracle.c for the definition it implements (SURVEY.md §8(c) c-1/c-2,
-PAPER.md:38, :54, :183-185, :203) and oracle/brute.py for the independent brute-force pin.
+PAPER.md:38, :54, :183-185, :203) and tests/brute_force.py for the independent brute-force pin.
 """
 from __future__ import annotations
 
@@ -51,7 +51,7 @@ def lib():
         L.oracle_grid_slab_counts.argtypes = [vp, vp]
         L.oracle_grid_get.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
         L.oracle_grid_get.restype = ctypes.c_int
-        L.oracle_trace.argtypes = [vp, vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int]
+        L.oracle_trace.argtypes = [vp, vp, ctypes.c_int64, vp, vp, vp, vp, vp, ctypes.c_int]
         L.oracle_trace.restype = ctypes.c_int64
         L.oracle_max_threads.restype = ctypes.c_int
         _lib = L
@@ -96,16 +96,18 @@ class Grid:
 
     def trace(self, rays: np.ndarray, nthreads: int = 0, with_steps: bool = False):
         """rays: (n, 8) float32 (vf_ray layout). Returns dict(xyz (n,3) int32, t (n,) float32,
-        status (n,) uint8: 0 miss / 1 hit / 2 non-canonical, steps (n,) int64 optional)."""
+        status (n,) uint8: 0 miss / 1 hit / 2 non-canonical, normal (n,3) int8 entry face,
+        steps (n,) int64 optional)."""
         r = np.ascontiguousarray(rays, dtype=np.float32).reshape(-1, 8)
         n = len(r)
         xyz = np.empty((n, 3), dtype=np.int32)
         t = np.empty(n, dtype=np.float32)
         st = np.empty(n, dtype=np.uint8)
         steps = np.empty(n, dtype=np.int64) if with_steps else None
+        normal = np.empty((n, 3), dtype=np.int8)
         lib().oracle_trace(self._p, r.ctypes.data, n, xyz.ctypes.data, t.ctypes.data, st.ctypes.data,
-                           steps.ctypes.data if steps is not None else None, nthreads)
-        out = dict(xyz=xyz, t=t, status=st)
+                           steps.ctypes.data if steps is not None else None, normal.ctypes.data, nthreads)
+        out = dict(xyz=xyz, t=t, status=st, normal=normal)
         if steps is not None:
             out["steps"] = steps
         return out

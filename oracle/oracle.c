@@ -308,7 +308,11 @@ static float tfloat(const etime* t) {
 
 /* ------------------------------------------------------------------ one ray (steps 3-6) */
 /* status: 0 miss, 1 hit, 2 ray outside the canonical domain */
-static int trace_one(const oracle_grid* g, const float* ray, int32_t* xyz, float* tout, int64_t* steps) {
+/* entry_axes: on a hit, the set of axes whose plane crossing entered the hit cell at t_hit (the
+ * stepped axes of the last step, or the root-box entry axes when the hit cell is the first one
+ * and t_start is a box-entry event later than tmin); 0 when the segment starts inside it. */
+static int trace_one(const oracle_grid* g, const float* ray, int32_t* xyz, float* tout, int64_t* steps,
+                     int* entry_axes) {
   const float o[3] = {ray[0], ray[1], ray[2]};
   const float d[3] = {ray[4], ray[5], ray[6]};
   const float tmin = ray[3], tmax = ray[7];
@@ -343,6 +347,7 @@ static int trace_one(const oracle_grid* g, const float* ray, int32_t* xyz, float
     if (tcmp(&ex, &te) < 0) te = ex;
   }
   if (tcmp(&ts, &te) >= 0) return 0;
+  int last_axes = 0; /* axes whose voxel-slab entry plane is crossed exactly at the current t */
 
   /* step 4: entry cell tau_b(t_start+) by binary search over plane indices */
   int64_t cell[3];
@@ -371,6 +376,19 @@ static int trace_one(const oracle_grid* g, const float* ray, int32_t* xyz, float
     cell[b] = lo;
   }
 
+  /* entry face of the first cell: every axis whose voxel-slab entry plane (d>0: plane cell,
+   * d<0: plane cell+1) is crossed exactly at t_start, provided t_start > tmin (otherwise the
+   * segment starts inside the cell) */
+  {
+    etime tm = scalar_time(TMIN);
+    if (tcmp(&ts, &tm) > 0)
+      for (int a = 0; a < 3; ++a) {
+        if (D[a] == 0) continue;
+        etime en = plane_time(D[a] > 0 ? cell[a] : cell[a] + 1, O[a], D[a]);
+        if (tcmp(&en, &ts) == 0) last_axes |= 1 << a;
+      }
+  }
+
   /* step 5: walk */
   etime tcur = ts;
   int64_t n = 0;
@@ -385,6 +403,7 @@ static int trace_one(const oracle_grid* g, const float* ray, int32_t* xyz, float
       xyz[2] = (int32_t)cell[2];
       *tout = tfloat(&tcur); /* step 6 */
       if (steps) *steps = n;
+      if (entry_axes) *entry_axes = last_axes;
       return 1;
     }
     etime nx[3];
@@ -403,8 +422,12 @@ static int trace_one(const oracle_grid* g, const float* ray, int32_t* xyz, float
       if (steps) *steps = n;
       return 0;
     }
+    last_axes = 0;
     for (int a = 0; a < 3; ++a)
-      if (D[a] != 0 && tcmp(&nx[a], &best) == 0) cell[a] += D[a] > 0 ? 1 : -1;
+      if (D[a] != 0 && tcmp(&nx[a], &best) == 0) {
+        cell[a] += D[a] > 0 ? 1 : -1;
+        last_axes |= 1 << a;
+      }
     tcur = best;
   }
 }
@@ -412,8 +435,9 @@ static int trace_one(const oracle_grid* g, const float* ray, int32_t* xyz, float
 /* rays: n x 8 floats (vf_ray layout). Outputs: xyz n x 3 (-1 on miss), t (+inf on miss),
  * status n (0 miss, 1 hit, 2 non-canonical), steps n (cells visited; may be NULL).
  * Returns the number of non-canonical rays. */
+/* normal: optional n x 3 int8 entry-face normal (-sign(d_a) on the lowest entry axis, else 0) */
 int64_t oracle_trace(const oracle_grid* g, const float* rays, int64_t n, int32_t* xyz, float* t, uint8_t* status,
-                     int64_t* steps, int nthreads) {
+                     int64_t* steps, int8_t* normal, int nthreads) {
   if (nthreads <= 0) nthreads = omp_get_max_threads();
   int64_t bad = 0;
 #pragma omp parallel for schedule(dynamic, 256) num_threads(nthreads) reduction(+ : bad)
@@ -421,7 +445,8 @@ int64_t oracle_trace(const oracle_grid* g, const float* rays, int64_t n, int32_t
     int32_t h[3] = {-1, -1, -1};
     float tt = INFINITY;
     int64_t s = 0;
-    int st = trace_one(g, rays + 8 * i, h, &tt, &s);
+    int ax = 0;
+    int st = trace_one(g, rays + 8 * i, h, &tt, &s, &ax);
     if (st != 1) {
       h[0] = h[1] = h[2] = -1;
       tt = INFINITY;
@@ -433,6 +458,13 @@ int64_t oracle_trace(const oracle_grid* g, const float* rays, int64_t n, int32_t
     t[i] = tt;
     if (status) status[i] = (uint8_t)st;
     if (steps) steps[i] = s;
+    if (normal) {
+      normal[3 * i] = normal[3 * i + 1] = normal[3 * i + 2] = 0;
+      if (st == 1 && ax) {
+        const int a = __builtin_ctz(ax);
+        normal[3 * i + a] = rays[8 * i + 4 + a] > 0.0f ? -1 : 1;
+      }
+    }
   }
   return bad;
 }

@@ -115,6 +115,22 @@ vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* h
   return launch_trace(h, rays, n, hits, trace_flags, (cudaStream_t)cuda_stream);
 }
 
+vf_status vf_trace_ex(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, vf_payload* payload,
+                      uint32_t trace_flags, void* cuda_stream) {
+  clear_error();
+  if (!h) {
+    set_error("vf_trace_ex: null handle");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (n == 0) return VF_OK;
+  if (!rays || !hits || !aligned16(rays) || !aligned16(hits) || ((uintptr_t)payload & 7u)) {
+    set_error("vf_trace_ex: rays/hits must be 16-byte aligned device pointers, payload 8-byte aligned");
+    return VF_ERR_INVALID_ARG;
+  }
+  DeviceGuard g(h->device);
+  return launch_trace(h, rays, n, hits, trace_flags, (cudaStream_t)cuda_stream, nullptr, payload);
+}
+
 vf_status vf_trace_counters(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t trace_flags,
                             void* cuda_stream, uint64_t counters[VF_NCOUNTERS]) {
   clear_error();

@@ -599,6 +599,44 @@ struct Lane {
   }
 
   __device__ __forceinline__ int4 hit_record() const { return make_int4(V[0], V[1], V[2], __float_as_int(E.t)); }
+
+  // Closest-hit payload (the paper's closest-hit shader): the hit
+  // voxel's terminating integer (its RGBA) and the entry-face normal -sign(d_a) e_a of the
+  // axis whose plane event entered the hit cell (lowest axis on exact ties; 0 when the segment
+  // starts inside the hit cell at tmin). Evaluated once per hit, at the finest tier.
+  __device__ __forceinline__ uint2 payload_record(const uint32_t* __restrict__ buf) const {
+    const uint32_t lx = ((uint32_t)V[0] >> lc) & msk, ly = ((uint32_t)V[1] >> lc) & msk,
+                   lz = ((uint32_t)V[2] >> lc) & msk;
+    uint32_t rgba = 0;
+    if (kind == K_RAW) {
+      const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
+      rgba = __ldg(buf + (size_t)N + lin * (df ? 2u : 1u));
+    } else {
+      const uint32_t lin = lx + (ly << sx) + (lz << sxy);
+      const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
+      if (kind == K_SVO)
+        rgba = __ldg(buf + hd.base + 2u * rank);
+      else if (kind == K_SVDAG)
+        rgba = __ldg(buf + __ldg(buf + hd.base + 1u + rank));
+      else
+        rgba = __ldg(buf + hd.base + rank);
+    }
+    uint32_t nrm = 0;
+    if (E.axis != TMIN_AXIS) {
+      // every axis whose voxel-slab entry plane is crossed exactly at E entered the cell (a finer
+      // plane may coincide with the event of a coarse step): exact comparisons, lowest axis wins
+      int a = E.axis;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        if (b >= a || !((moving >> b) & 1)) continue;
+        const int plane = ((dneg >> b) & 1) ? V[b] + 1 : V[b];
+        if (cmp_ep(r, E, b, plane) == 0) a = b;
+      }
+      const uint32_t v = sel3(r.d, a) > 0.f ? 0xFFu : 0x01u;  // int8 -1 or +1
+      nrm = v << (8 * a);
+    }
+    return make_uint2(rgba, nrm);
+  }
 };
 
 __device__ __forceinline__ int4 miss_record() { return make_int4(-1, -1, -1, 0x7f800000); }
@@ -626,10 +664,12 @@ __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const Tra
       } while (res == IT_CONTINUE);
       if (res == IT_HIT) {
         out = L.hit_record();
+        if (p.payload) p.payload[gid] = L.payload_record(buf);
         ct.add(VF_CTR_HITS);
       }
     }
     hits[gid] = out;
+    if (p.payload && out.x < 0) p.payload[gid] = make_uint2(0u, 0u);
     ct.add(VF_CTR_RAYS);
   }
   ct.flush(counters);
@@ -669,8 +709,10 @@ __global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceP
           ct.add(VF_CTR_RAYS);
           if (L.start(p, buf, __ldg(rays + 2 * idx), __ldg(rays + 2 * idx + 1), ct))
             active = true;
-          else
+          else {
             hits[idx] = miss_record();
+            if (p.payload) p.payload[idx] = make_uint2(0u, 0u);
+          }
         }
       }
       idle = __ballot_sync(0xffffffffu, !active);
@@ -684,6 +726,7 @@ __global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceP
       if (res != IT_CONTINUE) {
         if (res == IT_HIT) ct.add(VF_CTR_HITS);
         hits[idx] = res == IT_HIT ? L.hit_record() : miss_record();
+        if (p.payload) p.payload[idx] = res == IT_HIT ? L.payload_record(buf) : make_uint2(0u, 0u);
         active = false;
       }
     }
@@ -805,7 +848,7 @@ int persistent_blocks(KernelFn fn, int device) {
 }  // namespace
 
 vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags, cudaStream_t s,
-                       unsigned long long* counters) {
+                       unsigned long long* counters, vf_payload* payload) {
   if (n == 0) return VF_OK;
   uint32_t kinds = 0;
   for (uint32_t t = 0; t < h->fmt.n_tiers; ++t) kinds |= 1u << h->fmt.tiers[t].kind;
@@ -822,6 +865,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
       return (v >= 1 && v <= 32) ? v : 0;
     }();
     TraceParams tp = h->tp;
+    tp.payload = reinterpret_cast<uint2*>(payload);
     if (refill_env) tp.refill = (uint32_t)refill_env;
     const uint32_t slot = h->work_slot.fetch_add(1) % kWorkSlots;
     unsigned long long* work = h->work + 2 * slot;
@@ -839,7 +883,9 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
       set_error("vf_trace: %llu rays exceed one launch", (unsigned long long)n);
       return VF_ERR_INVALID_ARG;
     }
-    fn<<<(unsigned)blocks, threads, 0, s>>>(h->tp, h->buf, reinterpret_cast<const float4*>(rays),
+    TraceParams tp = h->tp;
+    tp.payload = reinterpret_cast<uint2*>(payload);
+    fn<<<(unsigned)blocks, threads, 0, s>>>(tp, h->buf, reinterpret_cast<const float4*>(rays),
                                             reinterpret_cast<int4*>(hits), n, counters, nullptr);
   }
   cudaError_t e = cudaGetLastError();

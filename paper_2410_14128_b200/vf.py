@@ -72,6 +72,7 @@ _sig = {
                   ctypes.POINTER(_u64)], ctypes.c_int),
     "vf_trace": ([_vp, _vp, _u64, _vp, _u32, _vp], ctypes.c_int),
     "vf_trace_host": ([_vp, _vp, _u64, _vp, _u32, _vp], ctypes.c_int),
+    "vf_trace_ex": ([_vp, _vp, _u64, _vp, _vp, _u32, _vp], ctypes.c_int),
     "vf_trace_counters": ([_vp, _vp, _u64, _vp, _u32, _vp, ctypes.POINTER(_u64)], ctypes.c_int),
     "vf_query": ([_vp, _vp, _u64, _vp, _vp], ctypes.c_int),
     "vf_stats_get": ([_vp, ctypes.POINTER(Stats)], ctypes.c_int),
@@ -205,6 +206,18 @@ class Handle:
         _check(_lib.vf_trace(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
                              self._flags(restart, persistent), _stream_ptr(stream)))
         return hits
+
+    def trace_payload(self, rays, hits=None, payload=None, restart: bool = False, stream=None):
+        """vf_trace_ex: hits plus closest-hit payload (n, 2) int32 {rgba, packed int8 normal}."""
+        import torch
+        n = rays.shape[0]
+        if hits is None:
+            hits = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        if payload is None:
+            payload = torch.empty((n, 2), dtype=torch.int32, device=rays.device)
+        _check(_lib.vf_trace_ex(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
+                                ctypes.c_void_p(payload.data_ptr()), self._flags(restart), _stream_ptr(stream)))
+        return hits, payload
 
     def counters(self, rays, hits=None, restart: bool = False, stream=None, persistent: bool = False) -> dict:
         """Run the counting variant of the trace kernel once; totals over all rays (synchronous)."""

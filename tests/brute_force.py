@@ -51,6 +51,7 @@ def first_hit(occ: np.ndarray, ray) -> tuple:
     for x, y, z in zip(xs.tolist(), ys.tolist(), zs.tolist()):
         lo, hi = tmin, tmax
         ok = True
+        enters = {}
         for a, v in enumerate((x, y, z)):
             e = iv[a].get(v)
             if e is None:
@@ -58,6 +59,7 @@ def first_hit(occ: np.ndarray, ray) -> tuple:
                 break
             if e == "all":
                 continue
+            enters[a] = e[0]
             if e[0] > lo:
                 lo = e[0]
             if hi is None or e[1] < hi:
@@ -67,14 +69,19 @@ def first_hit(occ: np.ndarray, ray) -> tuple:
         if hi is not None and not (lo < hi):
             continue
         if best is None or lo < best[3]:
-            best = (x, y, z, lo)
+            # entry face: axes whose slab is entered exactly at the entry time, unless the
+            # segment starts inside the voxel (entry time == tmin)
+            axes = [a for a, t in enters.items() if t == lo and lo > tmin]
+            best = (x, y, z, lo, axes)
     return best
 
 
-def trace(occ: np.ndarray, rays: np.ndarray):
-    """Vectorised convenience wrapper: returns (xyz (n,3) int, t_exact list[Fraction|None])."""
+def trace(occ: np.ndarray, rays: np.ndarray, with_normal: bool = False):
+    """Convenience wrapper: (xyz (n,3) int, t_exact list[Fraction|None][, normal (n,3) int8]).
+    normal = -sign(d_a) on the lowest entry axis, 0 when starting inside the hit voxel."""
     rays = np.asarray(rays, dtype=np.float32).reshape(-1, 8)
     xyz = np.full((len(rays), 3), -1, dtype=np.int64)
+    nrm = np.zeros((len(rays), 3), dtype=np.int8)
     ts = []
     for i, r in enumerate(rays):
         h = first_hit(occ, r)
@@ -83,4 +90,7 @@ def trace(occ: np.ndarray, rays: np.ndarray):
         else:
             xyz[i] = h[:3]
             ts.append(h[3])
-    return xyz, ts
+            if h[4]:
+                a = min(h[4])
+                nrm[i, a] = -1 if r[4 + a] > 0 else 1
+    return (xyz, ts, nrm) if with_normal else (xyz, ts)

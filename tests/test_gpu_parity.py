@@ -232,7 +232,7 @@ FULL = [
     ("cfg3", "G(10)"),
     ("cfg4", "R(4, 4, 4) G(7)"), ("cfg4", "R(3, 3, 3) G(8)"), ("cfg4", "S(11)"), ("cfg4", "R(1, 1, 1) T(2, 5)"),
     ("cfg4", "T(2, 4) R(3, 3, 3)"), ("cfg4", "R(11, 11, 11)"),
-    ("cfg5", "R(4, 4, 4) G(8)"), ("cfg5", "T(2, 6)"),
+    ("cfg5", "R(4, 4, 4) G(8)"), ("cfg5", "T(2, 6)"), ("cfg4i", "R(4, 4, 4) G(7)"), ("cfg4i", "S(11)"),
 ]
 
 
@@ -344,3 +344,29 @@ def test_table2_formats_parity(res):
             out = h.trace(rt, restart=restart).cpu().numpy()
             assert_parity(out[idx, :3], out[idx, 3].view(np.float32), ref, f"Table 2 row {label} {sig} restart={restart}")
         h.close()
+
+
+# ---------------------------------------------------------------- closest-hit payload (NEXT 4)
+@pytest.mark.parametrize("fmt", ["R(4, 4, 4)", "G(4)", "S(2) R(2^3)", "T(2, 2)", "R(1^3) D(3^3, 3)", "G(2) T(1, 2)"])
+def test_payload_rgba_and_entry_face(fmt):
+    """rgba = the stored voxel at the hit (the dense grid); normal = the oracle's entry face
+    (pinned to the brute force's geometric definition)."""
+    import torch
+    vf = _vf()
+    dims = (16, 16, 16)
+    d = inputs.random_occupancy(dims, 0.1, 8)
+    dense = inputs.dense_host(d)
+    h = vf.build(torch.from_numpy(dense.view(np.int32)).cuda(), fmt)
+    rays = _rays_small(dims, 17)
+    ref = oracle.Grid.from_generator(d).trace(rays)
+    rt = torch.from_numpy(rays).cuda()
+    for restart in (False, True):
+        hits, pay = h.trace_payload(rt, restart=restart)
+        hits, pay = hits.cpu().numpy(), pay.cpu().numpy()
+        assert_parity(hits[:, :3], hits[:, 3].view(np.float32), ref, fmt)
+        hit = ref["xyz"][:, 0] >= 0
+        x, y, z = ref["xyz"][hit].T
+        np.testing.assert_array_equal(np.ascontiguousarray(pay[hit, 0]).view(np.uint32), dense[z, y, x])
+        assert (pay[~hit] == 0).all()
+        nrm = np.ascontiguousarray(pay[:, 1]).view(np.uint8).reshape(-1, 4)[:, :3].view(np.int8)
+        np.testing.assert_array_equal(nrm, ref["normal"])

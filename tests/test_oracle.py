@@ -31,8 +31,9 @@ def _check_vs_brute(d, rays):
     g = oracle.Grid.from_generator(d)
     out = g.trace(rays)
     assert (out["status"] != 2).all(), "adversarial generator produced non-canonical rays"
-    bx, bt = brute_force.trace(occ, rays)
+    bx, bt, bn = brute_force.trace(occ, rays, with_normal=True)
     np.testing.assert_array_equal(out["xyz"], bx.astype(np.int32))
+    np.testing.assert_array_equal(out["normal"], bn)
     for i, te in enumerate(bt):
         if te is None:
             assert math.isinf(out["t"][i])

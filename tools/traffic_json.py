@@ -18,7 +18,8 @@ for r in rows[hi + 1:]:
         continue
     v = float(d["Metric Value"].replace(",", ""))
     unit = d["Metric Unit"]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6}.get(unit, 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6,
+             "inst": 1, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9}.get(unit, 1)
     launch.setdefault(int(d["ID"]), {})[d["Metric Name"]] = v * scale
 keys = [l.split(" ", 1)[1].strip() for l in open(sys.argv[2]) if l.startswith("LAUNCH ")]
 ids = sorted(launch)
@@ -28,6 +29,8 @@ for key, i in zip(keys, ids):
     m = launch[i]
     tj[key] = {"dram_bytes_per_launch": int(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)),
                "ncu_duration_ns": int(m.get("gpu__time_duration.sum", 0)),
+               "warp_inst_per_launch": int(m.get("smsp__inst_executed.sum", 0)),
+               "thread_inst_per_launch": int(m.get("smsp__thread_inst_executed.sum", 0)),
                "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
                          "--clock-control none over tools/sweep_trace.py (cold cache, serialised)"}
 json.dump(tj, open(path, "w"), indent=1, sort_keys=True)
