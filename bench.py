@@ -216,8 +216,10 @@ def run_ours(args):
 
     counts = shard.shard_counts(perm, width, world)
 
+    incoh = CONFIGS[cfg][1] == "incoherent"  # VF_TRACE_INCOHERENT hint for secondary-style rays
+
     def step():
-        handle.trace(rays, hits, restart=args.restart)
+        handle.trace(rays, hits, restart=args.restart, incoherent=incoh)
 
     def gather():  # the one collective: hit buffers to rank 0 (NCCL)
         if world > 1:
@@ -266,13 +268,13 @@ def run_ours(args):
         hr = torch.from_numpy(np.ascontiguousarray(rays_all[own])).pin_memory()
         hh = torch.empty((n_local, 4), dtype=torch.int32).pin_memory()
         for _ in range(2):
-            handle.trace_host(hr, hh, restart=args.restart)
+            handle.trace_host(hr, hh, restart=args.restart, incoherent=incoh)
         e2e = []
         for _ in range(max(3, min(args.steps, 10))):
             flush.fill_(1)
             torch.cuda.synchronize()
             t1 = time.perf_counter()
-            handle.trace_host(hr, hh, restart=args.restart)
+            handle.trace_host(hr, hh, restart=args.restart, incoherent=incoh)
             e2e.append(time.perf_counter() - t1)
         e2e_val = n_local / statistics.median(e2e) / 1e6 * world
 
@@ -329,7 +331,7 @@ def run_ours(args):
             "ms_per_step": round(tot_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{cfg}: {desc}", "format": handle.signature, "variant":
-                       "restart" if args.restart else "stack", "volume": list(dims), "rays": n_total,
+                       ("restart" if args.restart else "stack") + ("+incoherent" if incoh else ""), "volume": list(dims), "rays": n_total,
                        "nonempty_voxels": int(nonempty), "bytes_used": stats["bytes_used"],
                        "paper_layout_bytes": stats["paper_layout_bytes"], "bytes_per_voxel": round(bpv, 4),
                        "bytes_per_voxel_paper": round(stats["paper_layout_bytes"] / max(nonempty, 1), 4),
@@ -378,6 +380,7 @@ def sweep(cfg, vol, rays, hits, stream, flush, args, ref_idx=None, ref=None):
         traffic = {}
     out = []
     n = rays.shape[0]
+    incoh = CONFIGS[cfg][1] == "incoherent"
     for fmt in SWEEP[cfg]:
         try:
             h = vf.build((keys, rgba, dims), fmt)
@@ -394,13 +397,13 @@ def sweep(cfg, vol, rays, hits, stream, flush, args, ref_idx=None, ref=None):
             c = h.counters(rays, hits, restart=restart)
             alg = 48 * n + c["format_bytes"]
             for _ in range(3):
-                h.trace(rays, hits, restart=restart)
+                h.trace(rays, hits, restart=restart, incoherent=incoh)
             ms = []
             for i in range(7):
                 flush.fill_(i)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                h.trace(rays, hits, restart=restart)
+                h.trace(rays, hits, restart=restart, incoherent=incoh)
                 b.record(stream)
                 torch.cuda.synchronize()
                 ms.append(a.elapsed_time(b))

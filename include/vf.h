@@ -143,10 +143,15 @@ typedef struct {
 } vf_hit; /* 16 B; miss: x = y = z = -1, t = +inf */
 
 enum {
-  VF_TRACE_RESTART_SV = 1u << 0 /* "restarting sparse voxel intersection" (§4.3):
+  VF_TRACE_RESTART_SV = 1u << 0, /* "restarting sparse voxel intersection" (§4.3):
                                    stackless — after leaving a node of an SVO / SVDAG / N^3-tree
                                    level, re-descend from that level's sub-volume root instead
                                    of popping a per-thread stack. Results are identical. */
+  VF_TRACE_INCOHERENT = 1u << 1, /* hint: the rays are incoherent (secondary / random rays). The
+                                   trace then runs persistent warps that refill finished lanes
+                                   with new rays (one atomic per batch), recovering the SIMT lanes
+                                   a warp otherwise idles while its longest ray finishes. Results
+                                   are identical; coherent primary rays are faster without it. */
   /* bit 30 is reserved (internal ablation: persistent warps with dynamic ray refill) */
 };
 

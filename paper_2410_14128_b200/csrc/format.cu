@@ -315,7 +315,7 @@ TraceParams make_trace_params(const Format& f, uint32_t root) {
   }
   p.n_tiers = f.n_tiers;
   p.root = root;
-  p.refill = 12;
+  p.refill = 16;  // A/B on incoherent rays (cfg4i): 16 best of 8/16/24/32
   return p;
 }
 

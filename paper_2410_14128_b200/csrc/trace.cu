@@ -852,7 +852,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
   if (n == 0) return VF_OK;
   uint32_t kinds = 0;
   for (uint32_t t = 0; t < h->fmt.n_tiers; ++t) kinds |= 1u << h->fmt.tiers[t].kind;
-  const bool persistent = (flags & VF_TRACE_PERSISTENT_WARPS) != 0;
+  const bool persistent = (flags & (VF_TRACE_PERSISTENT_WARPS | VF_TRACE_INCOHERENT)) != 0;
   KernelFn fn = select_kernel(kinds, (flags & VF_TRACE_RESTART_SV) != 0, counters != nullptr, persistent);
   if (!fn) {
     set_error("vf_trace: no kernel instantiated for kind set 0x%x", kinds);

@@ -27,6 +27,7 @@ VF_VOL_DENSE_DEVICE, VF_VOL_SPARSE_DEVICE = 0, 1
 VF_BUILD_WHOLE_LEVEL_DEDUP = 1
 VF_BUILD_DEFAULT = VF_BUILD_WHOLE_LEVEL_DEDUP
 VF_TRACE_RESTART_SV = 1
+VF_TRACE_INCOHERENT = 2
 VF_TRACE_PERSISTENT_WARPS = 1 << 30  # internal ablation flag (include/vf.h: bit 30 reserved)
 VF_MAX_LEVELS = 16
 VF_MAX_TIERS = 16
@@ -191,10 +192,12 @@ class Handle:
 
     # -- the hot path
     @staticmethod
-    def _flags(restart, persistent=False):
-        return (VF_TRACE_RESTART_SV if restart else 0) | (VF_TRACE_PERSISTENT_WARPS if persistent else 0)
+    def _flags(restart, persistent=False, incoherent=False):
+        return ((VF_TRACE_RESTART_SV if restart else 0) | (VF_TRACE_PERSISTENT_WARPS if persistent else 0)
+                | (VF_TRACE_INCOHERENT if incoherent else 0))
 
-    def trace(self, rays, hits=None, restart: bool = False, stream=None, persistent: bool = False):
+    def trace(self, rays, hits=None, restart: bool = False, stream=None, persistent: bool = False,
+              incoherent: bool = False):
         """rays: (n, 8) float32 CUDA tensor (vf_ray); hits: (n, 4) int32 CUDA tensor (vf_hit, t as
         float bits). Asynchronous on `stream`. Returns hits."""
         import torch
@@ -204,7 +207,7 @@ class Handle:
         assert rays.is_cuda and rays.dtype == torch.float32 and rays.is_contiguous() and rays.shape[1] == 8
         assert hits.is_cuda and hits.dtype == torch.int32 and hits.is_contiguous() and hits.shape[0] >= n
         _check(_lib.vf_trace(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
-                             self._flags(restart, persistent), _stream_ptr(stream)))
+                             self._flags(restart, persistent, incoherent), _stream_ptr(stream)))
         return hits
 
     def trace_payload(self, rays, hits=None, payload=None, restart: bool = False, stream=None):
@@ -219,7 +222,8 @@ class Handle:
                                 ctypes.c_void_p(payload.data_ptr()), self._flags(restart), _stream_ptr(stream)))
         return hits, payload
 
-    def counters(self, rays, hits=None, restart: bool = False, stream=None, persistent: bool = False) -> dict:
+    def counters(self, rays, hits=None, restart: bool = False, stream=None, persistent: bool = False,
+                 incoherent: bool = False) -> dict:
         """Run the counting variant of the trace kernel once; totals over all rays (synchronous)."""
         import torch
         n = rays.shape[0]
@@ -227,14 +231,14 @@ class Handle:
             hits = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
         c = (_u64 * VF_NCOUNTERS)()
         _check(_lib.vf_trace_counters(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
-                                      self._flags(restart, persistent), _stream_ptr(stream), c))
+                                      self._flags(restart, persistent, incoherent), _stream_ptr(stream), c))
         return {k: int(c[i]) for i, k in enumerate(COUNTER_NAMES)}
 
-    def trace_host(self, rays, hits, restart: bool = False, stream=None):
+    def trace_host(self, rays, hits, restart: bool = False, stream=None, incoherent: bool = False):
         """End to end: host (pinned) rays (n,8) float32 -> host hits (n,4) int32, copies inside."""
         n = rays.shape[0]
         _check(_lib.vf_trace_host(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
-                                  VF_TRACE_RESTART_SV if restart else 0, _stream_ptr(stream)))
+                                  self._flags(restart, False, incoherent), _stream_ptr(stream)))
         return hits
 
     def query(self, xyz, stream=None):
