@@ -259,7 +259,7 @@ def test_full_size_sampled(cfg, fmt):
     ref = oracle.Grid.procedural(vol).trace(sample)
     rt = torch.from_numpy(rays).cuda()
     for restart in (False, True):
-        out = h.trace(rt, restart=restart).cpu().numpy()  # the full frame, as bench.py launches it
+        out = h.trace(rt, restart=restart, incoherent=(cfg == "cfg4i")).cpu().numpy()  # as bench.py launches it
         xyz, t = out[idx, :3], out[idx, 3].view(np.float32)
         if cfg == "cfg4":
             x2, t2 = gpu_trace(h, sample[len(idx):], restart)
