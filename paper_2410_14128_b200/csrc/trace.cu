@@ -243,6 +243,9 @@ __device__ __forceinline__ bool has_kind(uint32_t k) {
 }
 
 // Node header registers for the current tier.
+#ifndef VF_DESCEND_LOOP
+#define VF_DESCEND_LOOP 0  // 1: descend repeatedly inside one iterate() call (A/B)
+#endif
 #ifndef VF_SVDAG_WIDE
 #define VF_SVDAG_WIDE 0  // 1: 2 x LDG.128 SVDAG headers (A/B: slower, +50 registers)
 #endif
@@ -428,6 +431,9 @@ struct Lane {
   // A pop always follows a step, so it lands on a new cell.
   __device__ __forceinline__ int iterate(const TraceParams& p, const uint32_t* __restrict__ buf,
                                          uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
+#if VF_DESCEND_LOOP
+   for (;;) {
+#endif
     int nt = t;       // tier after this iteration
     uint32_t nN = N;  // node after this iteration
     {
@@ -510,11 +516,20 @@ struct Lane {
     if (nt < 0) return IT_MISS;
     // tier change (descent or pop), shared by both paths so a warp mixing them runs it once
     if (nt != t) {
+#if VF_DESCEND_LOOP
+      const bool descended = nt > t;
+#endif
       set_tier(p, nt);
       N = nN;
       hd = load_header<KINDS>(buf, kind, N, ct);
+#if VF_DESCEND_LOOP
+      if (descended) continue;  // test the child's cell in the same iteration: one step per call
+#endif
     }
     return IT_CONTINUE;
+#if VF_DESCEND_LOOP
+   }
+#endif
   }
 
   // -- step: exact next event among the three axes at this tier's cell size. Sets nt < 0 when

@@ -31,7 +31,8 @@ for key, i in zip(keys, ids):
                "ncu_duration_ns": int(m.get("gpu__time_duration.sum", 0)),
                "warp_inst_per_launch": int(m.get("smsp__inst_executed.sum", 0)),
                "thread_inst_per_launch": int(m.get("smsp__thread_inst_executed.sum", 0)),
-               "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
+               "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+                         "smsp__inst_executed.sum,smsp__thread_inst_executed.sum "
                          "--clock-control none over tools/sweep_trace.py (cold cache, serialised)"}
 json.dump(tj, open(path, "w"), indent=1, sort_keys=True)
 print(f"{len(keys)} launches merged into {path}")
