@@ -313,6 +313,16 @@ TraceParams make_trace_params(const Format& f, uint32_t root) {
     p.lf0[a] = f.tiers[0].lf[a];
     p.dims[a] = (int32_t)f.dims[a];
   }
+  for (uint32_t t = 0; t < f.n_tiers; ++t) {
+    const Tier& T = f.tiers[t];
+    const uint32_t lcn = t + 1 < f.n_tiers ? f.tiers[t + 1].lc : 0;
+    const uint32_t lcp = t > 0 ? f.tiers[t - 1].lc : 15;
+    const uint32_t sx = T.lf[0], sxy = T.lf[0] + T.lf[1];
+    const uint32_t mb = t == 0 ? 12 : T.lf[0];
+    p.tword[t] = (T.kind << TW_KIND) | (T.lc << TW_LC) | (lcn << TW_LCN) | (lcp << TW_LCP) | (sx << TW_SX) |
+                 (sxy << TW_SXY) | (mb << TW_MB) | (T.last ? TW_LAST : 0u) |
+                 (t + 1 == f.n_tiers ? TW_FINEST : 0u) | (T.df ? TW_DF : 0u) | (T.top ? TW_TOP : 0u);
+  }
   p.n_tiers = f.n_tiers;
   p.root = root;
   p.refill = 16;  // A/B on incoherent rays (cfg4i): 16 best of 8/16/24/32

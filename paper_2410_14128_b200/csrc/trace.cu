@@ -96,115 +96,35 @@ __device__ __forceinline__ int cert(float t1, float t2) {
   return 2;
 }
 
-// sign(T_a(P) - T_b(Q)); t1 / t2 are the fp32 event values.
-__device__ __forceinline__ int cmp_pp(const Ray& r, int a, int P, float t1, int b, int Q, float t2) {
+// sign(T_a(P) - T_b(Q)) for two plane events on any axes (a == b compares the planes); t1 / t2
+// are their fp32 values. o / d are the ray's origin and direction (indexed at run time only here,
+// on the entry and slow paths).
+__device__ __forceinline__ int cmp_pp(const float (&o)[3], const float (&d)[3], int a, int P, float t1, int b, int Q,
+                                      float t2) {
   if (a == b) {
     const int s = (P > Q) - (P < Q);
-    return sel3(r.d, a) > 0.f ? s : -s;
+    return sel3(d, a) > 0.f ? s : -s;
   }
   const int c = cert(t1, t2);
   if (c != 2) return c;
-  return cmp_pp_exact(P, sel3(r.o, a), sel3(r.d, a), Q, sel3(r.o, b), sel3(r.d, b));
+  return cmp_pp_exact(P, sel3(o, a), sel3(d, a), Q, sel3(o, b), sel3(d, b));
 }
 
-// sign(E - T_b(Q)) for an event E (plane or tmin).
-__device__ __forceinline__ int cmp_ep(const Ray& r, const Event& E, int b, int Q) {
-  const float tq = tplane(Q, sel3(r.o, b), sel3(r.inv, b));
-  if (E.axis == TMIN_AXIS) {
-    const int c = cert(E.t, tq);
+// sign(E - F) for two events given as {axis, plane, fp32 time}; axis TMIN_AXIS = the scalar t.
+__device__ __forceinline__ int cmp_events(const float (&o)[3], const float (&d)[3], int ea, int eP, float et, int fa,
+                                          int fP, float ft) {
+  if (fa == TMIN_AXIS) {
+    if (ea == TMIN_AXIS) return (et > ft) - (et < ft);
+    const int c = cert(et, ft);
     if (c != 2) return c;
-    return -cmp_ps_exact(Q, sel3(r.o, b), sel3(r.d, b), E.t);
+    return cmp_ps_exact(eP, sel3(o, ea), sel3(d, ea), ft);
   }
-  return cmp_pp(r, E.axis, E.P, E.t, b, Q, tq);
-}
-
-// sign(E1 - E2) for two events.
-__device__ __forceinline__ int cmp_ee(const Ray& r, const Event& E1, const Event& E2) {
-  if (E2.axis == TMIN_AXIS) {
-    if (E1.axis == TMIN_AXIS) return 0;
-    const int c = cert(E1.t, E2.t);
+  if (ea == TMIN_AXIS) {
+    const int c = cert(et, ft);
     if (c != 2) return c;
-    return cmp_ps_exact(E1.P, sel3(r.o, E1.axis), sel3(r.d, E1.axis), E2.t);
+    return -cmp_ps_exact(fP, sel3(o, fa), sel3(d, fa), et);
   }
-  return cmp_ep(r, E1, E2.axis, E2.P);
-}
-
-// sign(E - s) for a scalar s (tmax).
-__device__ __forceinline__ int cmp_es(const Ray& r, const Event& E, float s) {
-  if (E.axis == TMIN_AXIS) return (E.t > s) - (E.t < s);
-  const int c = cert(E.t, s);
-  if (c != 2) return c;
-  return cmp_ps_exact(E.P, sel3(r.o, E.axis), sel3(r.d, E.axis), s);
-}
-
-// sign(E - T_b(Q)) with every operand passed as a scalar (for the out-of-line slow paths, so the
-// ray never has to be spilled to local memory for a call).
-__device__ __forceinline__ int cmp_ep_s(int eaxis, int eP, float et, float oa, float da, int b, int Q, float ob,
-                                        float db, float invb) {
-  if (eaxis == b) {
-    const int s = (eP > Q) - (eP < Q);
-    return db > 0.f ? s : -s;
-  }
-  const float tq = tplane(Q, ob, invb);
-  const int c = cert(et, tq);
-  if (c != 2) return c;
-  if (eaxis == TMIN_AXIS) return -cmp_ps_exact(Q, ob, db, et);
-  return cmp_pp_exact(eP, oa, da, Q, ob, db);
-}
-
-// Finest cell index on axis b at event E (right limit), known to lie in [lo, hi]:
-//   d_b > 0: T_b(k) <= E < T_b(k+1);   d_b < 0: T_b(k+1) <= E < T_b(k).
-// Slow path: candidate from fp32, then certified plane comparisons (planes lo / hi+1 are known
-// crossed / not crossed and are never compared). oa / da: origin / direction on E's axis.
-__device__ __forceinline__ int locate_slow(int b, float ob, float db, float invb, int eaxis, int eP, float et, float oa,
-                                        float da, int lo, int hi) {
-  const float x = fmaf(et, db, ob);
-  float kf = db > 0.f ? floorf(x) : ceilf(x) - 1.0f;
-  kf = fminf(fmaxf(kf, (float)lo), (float)hi);
-  int k = (int)kf;
-  if (db > 0.f) {
-    for (;;) {
-      if (k > lo && cmp_ep_s(eaxis, eP, et, oa, da, b, k, ob, db, invb) < 0) {
-        --k;
-        continue;
-      }
-      if (k < hi && cmp_ep_s(eaxis, eP, et, oa, da, b, k + 1, ob, db, invb) >= 0) {
-        ++k;
-        continue;
-      }
-      break;
-    }
-  } else {
-    for (;;) {
-      if (k < hi && cmp_ep_s(eaxis, eP, et, oa, da, b, k + 1, ob, db, invb) < 0) {
-        ++k;
-        continue;
-      }
-      if (k > lo && cmp_ep_s(eaxis, eP, et, oa, da, b, k, ob, db, invb) >= 0) {
-        --k;
-        continue;
-      }
-      break;
-    }
-  }
-  return k;
-}
-
-// Fast path: the position x = o_b + T_E d_b is computed as x^ = fma(T^_E, d_b, o_b) with
-// |x^ - x| <= 3.01u|T d_b| + 1.01u|x^| (T^_E has relative error <= 3u, one rounding in the fma),
-// so B = 2^-21 (|T^ d_b| + |x^|) >= 8u(...) bounds it with margin. If [x^-B, x^+B] contains no
-// integer, x is not on a plane and tau_b(E+) = floor(x) = floor(x^) for either sign of d_b.
-// Otherwise (ray on / near a plane at E: ~0.2% of calls) the certified slow path decides.
-__device__ __forceinline__ int locate(const Ray& r, const Event& E, int b, int lo, int hi) {
-  const float db = sel3(r.d, b), ob = sel3(r.o, b);
-  const float x = fmaf(E.t, db, ob);
-  const float fl = floorf(x);
-  const float f = x - fl;  // exact
-  const float B = (fabsf(E.t * db) + fabsf(x)) * 0x1p-21f;
-  const int k = (int)fl;
-  if (f > B && 1.0f - f > B && k >= lo && k <= hi) return k;
-  const int ea = E.axis > 2 ? 0 : E.axis;
-  return locate_slow(b, ob, db, sel3(r.inv, b), E.axis, E.P, E.t, sel3(r.o, ea), sel3(r.d, ea), lo, hi);
+  return cmp_pp(o, d, ea, eP, et, fa, fP, ft);
 }
 
 // Exact argmin of the three next-plane events (ties step together). c = candidate mask (>= 2
@@ -242,32 +162,13 @@ __device__ __forceinline__ bool has_kind(uint32_t k) {
   return (KINDS >> k) & 1u;
 }
 
+__device__ __forceinline__ uint32_t twf(uint32_t w, uint32_t pos, uint32_t len) { return (w >> pos) & ((1u << len) - 1u); }
+
 // Node header registers for the current tier.
-#ifndef VF_DESCEND_LOOP
-#define VF_DESCEND_LOOP 0  // 1: descend repeatedly inside one iterate() call (A/B)
-#endif
-#ifndef VF_SVDAG_WIDE
-#define VF_SVDAG_WIDE 0  // 1: 2 x LDG.128 SVDAG headers (A/B: slower, +50 registers)
-#endif
 struct Header {
   uint64_t mask;  // SVO/SVDAG: valid bits; N^3: 64-bit occupancy
   uint32_t base;  // SVO: first child; SVDAG: node address; N^3: children block
-#if VF_SVDAG_WIDE
-  // SVDAG: the two 16-B-aligned vectors covering the node header (paper layout, unpadded) —
-  // header at word k = N & 3, child pointers at k+1 .. 7 are then already in registers.
-  uint4 a, b;
-  uint32_t k;
-#endif
 };
-
-#if VF_SVDAG_WIDE
-// v[i] of the eight words {a.x..a.w, b.x..b.w}, i in [0, 8), without indexed memory.
-__device__ __forceinline__ uint32_t sel8(const uint4& a, const uint4& b, uint32_t i) {
-  const uint4 v = (i & 4u) ? b : a;
-  const uint32_t lo = (i & 1u) ? v.y : v.x, hi = (i & 1u) ? v.w : v.z;
-  return (i & 2u) ? hi : lo;
-}
-#endif
 
 // Per-ray work counters of the VF_COUNTERS variant (SURVEY.md §8(d) "Counts come from a
 // -DVF_COUNTERS build of the same kernel"). Compiled away when COUNT == false.
@@ -309,15 +210,7 @@ __device__ __forceinline__ Header load_header(const uint32_t* __restrict__ buf, 
     ct.add(VF_CTR_SVO_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 8);
   } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-#if VF_SVDAG_WIDE
-    const uint4* q = reinterpret_cast<const uint4*>(buf + (N & ~3u));
-    h.a = __ldg(q);
-    h.b = __ldg(q + 1);  // the buffer carries 8 guard words, so this never reads past the end
-    h.k = N & 3u;
-    h.mask = sel8(h.a, h.b, h.k) & 0xFFu;
-#else
     h.mask = __ldg(buf + N) & 0xFFu;
-#endif
     ct.add(VF_CTR_SVDAG_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 4);
   } else if (has_kind<KINDS>(K_NTREE) && kind == K_NTREE) {
@@ -334,94 +227,184 @@ enum { IT_CONTINUE = 0, IT_HIT = 1, IT_MISS = 2 };
 
 // The per-ray traversal state machine: start() is the root function, iterate() is one cell test
 // followed by either a descent or one DDA step (with pop / restart when the step leaves a node).
-// Per-tier parameters of the current tier are cached in registers and refreshed only when the
-// tier changes (descent, pop, restart).
+// The current tier's packed word (TraceParams::tword, staged in shared memory) and the fields
+// the cell test needs are cached in registers and refreshed only when the tier changes.
+//
+// The current event E (the time the ray entered the current cell) is {eaxis, et}: a plane event
+// on axis eaxis, or tmin (eaxis = TMIN_AXIS). Its plane is not stored: the cell entered through
+// it is V[eaxis], so the plane is V[eaxis] + (d < 0) — the event axis never goes stale, and
+// descents and pops do not move V. The exact fallbacks rebuild it from there.
 template <uint32_t KINDS, bool RESTART, bool COUNT>
 struct Lane {
-  Ray r;
-  Event E;
+  float o[3], d[3], inv[3];  // inv = RN(1/d); +inf on axes with d = 0 (their next plane is never)
+  float tmax;
   int V[3];       // finest voxel of the current cell (bits below lc(t) valid unless stale)
+  int eaxis;      // current event: axis of the plane crossed (TMIN_AXIS: the segment start)
+  float et;       // its fp32 time fl(fl(P - o) * inv) (or tmin)
   int t;          // current tier
   uint32_t N;     // current node (word address)
-  uint32_t kind;  // kind of tier t
+  uint32_t tw;    // tier word of tier t
+  uint32_t lc, msk, sx, sxy;  // decoded from tw
   Header hd;
-  int stale;   // axes whose bits below stale_lc are not exact at E
+  int stale;          // axes whose bits below stale_lc are not exact at E
   uint32_t stale_lc;  // bits of V below this are stale on the axes in `stale`
-  int moving;  // axes with d != 0
-  int dneg;    // axes with d < 0
+  int moving;         // axes with d != 0
+  int dneg;           // axes with d < 0
   bool tmax_finite;
-  // cached parameters of tier t
-  uint32_t lc, msk, sx, sxy;
-  bool last, finest, df;
   int budget;  // DF tier: remaining L1 distance within which every cell is known empty
   // (the per-tier node stack lives outside the struct so that the struct itself can stay in
   //  registers: an indexed member would force the whole object into local memory)
 
-  __device__ __forceinline__ void set_tier(const TraceParams& p, int nt) {
+  __device__ __forceinline__ int eplane() const { return sel3(V, eaxis) + ((dneg >> eaxis) & 1); }
+
+  // sign(E - T_b(Q)) for a moving axis b (a compile-time constant at every hot call site).
+  __device__ __forceinline__ int cmp_eq(int b, int Q) const {
+    // (sel3, not o[b]: an index the compiler cannot resolve would move the lane to local memory)
+    const float ob = sel3(o, b), db = sel3(d, b);
+    if (eaxis == b) {
+      const int P = sel3(V, b) + ((dneg >> b) & 1);
+      const int s = (P > Q) - (P < Q);
+      return db > 0.f ? s : -s;
+    }
+    const float tq = tplane(Q, ob, sel3(inv, b));
+    const int c = cert(et, tq);
+    if (c != 2) return c;
+    if (eaxis == TMIN_AXIS) return -cmp_ps_exact(Q, ob, db, et);
+    return cmp_pp_exact(eplane(), sel3(o, eaxis), sel3(d, eaxis), Q, ob, db);
+  }
+
+  // sign(E - s) for a scalar s (tmax).
+  __device__ __forceinline__ int cmp_es(float s) const {
+    if (eaxis == TMIN_AXIS) return (et > s) - (et < s);
+    const int c = cert(et, s);
+    if (c != 2) return c;
+    return cmp_ps_exact(eplane(), sel3(o, eaxis), sel3(d, eaxis), s);
+  }
+
+  // Finest cell index on axis b at the current event E (right limit), known to lie in [lo, hi]:
+  //   d_b > 0: T_b(k) <= E < T_b(k+1);   d_b < 0: T_b(k+1) <= E < T_b(k).
+  // Fast path: x = o_b + T_E d_b is computed as x^ = fma(T^_E, d_b, o_b) with
+  // |x^ - x| <= 3.01u|T d_b| + 1.01u|x^| (T^_E has relative error <= 3u, one rounding in the fma),
+  // so B = 2^-21 (|T^ d_b| + |x^|) >= 8u(...) bounds it with margin. If [x^-B, x^+B] contains no
+  // integer, x is not on a plane and tau_b(E+) = floor(x) = floor(x^) for either sign of d_b.
+  // Otherwise (ray on / near a plane at E: ~0.2% of calls) the candidate is corrected with
+  // certified plane comparisons (planes lo / hi+1 are known crossed / not crossed).
+  __device__ __forceinline__ int locate(int b, int lo, int hi) const {
+    const float db = sel3(d, b), ob = sel3(o, b);
+    const float x = fmaf(et, db, ob);
+    const float fl = floorf(x);
+    const float f = x - fl;  // exact
+    const float B = (fabsf(et * db) + fabsf(x)) * 0x1p-21f;
+    int k = (int)fl;
+    if (f > B && 1.0f - f > B && k >= lo && k <= hi) return k;
+    float kf = db > 0.f ? fl : ceilf(x) - 1.0f;
+    kf = fminf(fmaxf(kf, (float)lo), (float)hi);
+    k = (int)kf;
+    if (db > 0.f) {
+      for (;;) {
+        if (k > lo && cmp_eq(b, k) < 0) {
+          --k;
+          continue;
+        }
+        if (k < hi && cmp_eq(b, k + 1) >= 0) {
+          ++k;
+          continue;
+        }
+        break;
+      }
+    } else {
+      for (;;) {
+        if (k < hi && cmp_eq(b, k + 1) < 0) {
+          ++k;
+          continue;
+        }
+        if (k > lo && cmp_eq(b, k) >= 0) {
+          --k;
+          continue;
+        }
+        break;
+      }
+    }
+    return k;
+  }
+
+  __device__ __forceinline__ void set_tier(const uint32_t* s_tw, int nt) {
     t = nt;
-    kind = (p.kind_pack >> (2 * nt)) & 3u;
-    lc = field4(p.lc_pack, nt);
-    const uint32_t lf = field4(p.lf_pack, nt);
-    msk = nt == 0 ? 0xFFFFFFFFu : ((1u << lf) - 1u);
-    sx = nt == 0 ? p.lf0[0] : lf;
-    sxy = nt == 0 ? p.lf0[0] + p.lf0[1] : 2 * lf;
-    last = (p.last_mask >> nt) & 1u;
-    finest = nt == (int)p.n_tiers - 1;
-    df = (p.df_mask >> nt) & 1u;
+    tw = s_tw[nt];
+    lc = twf(tw, TW_LC, 4);
+    msk = (1u << twf(tw, TW_MB, 4)) - 1u;
+    sx = twf(tw, TW_SX, 4);
+    sxy = twf(tw, TW_SXY, 5);
     budget = 0;
   }
 
   // ---- root function: word 0, root-box test, exact entry cell ---------------
-  __device__ __forceinline__ bool start(const TraceParams& p, const uint32_t* __restrict__ buf, const float4 r0,
-                                        const float4 r1, Ctr<COUNT>& ct) {
-    r.o[0] = r0.x;
-    r.o[1] = r0.y;
-    r.o[2] = r0.z;
-    r.tmin = r0.w;
-    r.d[0] = r1.x;
-    r.d[1] = r1.y;
-    r.d[2] = r1.z;
-    r.tmax = r1.w;
-    tmax_finite = r.tmax < __int_as_float(0x7f800000);
+  __device__ __forceinline__ bool start(const TraceParams& p, const uint32_t* __restrict__ buf,
+                                        const uint32_t* s_tw, const float4 r0, const float4 r1, Ctr<COUNT>& ct) {
+    o[0] = r0.x;
+    o[1] = r0.y;
+    o[2] = r0.z;
+    const float tmin = r0.w;
+    d[0] = r1.x;
+    d[1] = r1.y;
+    d[2] = r1.z;
+    tmax = r1.w;
+    tmax_finite = tmax < __int_as_float(0x7f800000);
     if (p.root == 0) return false;  // empty volume: buffer [0]
     moving = 0;
     dneg = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      if (r.d[a] != 0.f) moving |= 1 << a;
-      if (r.d[a] < 0.f) dneg |= 1 << a;
-      r.inv[a] = r.d[a] != 0.f ? __frcp_rn(r.d[a]) : 0.f;
+      if (d[a] != 0.f) moving |= 1 << a;
+      if (d[a] < 0.f) dneg |= 1 << a;
+      inv[a] = d[a] != 0.f ? __frcp_rn(d[a]) : __int_as_float(0x7f800000);
     }
     if (!moving) return false;  // reading A5: all-zero direction misses
-    if (!(r.tmin < r.tmax) && tmax_finite) return false;
-    E = Event{TMIN_AXIS, 0, r.tmin};
+    if (!(tmin < tmax) && tmax_finite) return false;
+    // entry event: the latest of tmin and the entry planes of the moving slabs
+    int ea = TMIN_AXIS, eP = 0;
+    float te = tmin;
     bool miss = false;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (!((moving >> a) & 1)) {
         // half-open membership: floor(o_a) in [0, R_a)
-        if (!(r.o[a] >= 0.f && r.o[a] < (float)p.dims[a])) miss = true;
+        if (!(o[a] >= 0.f && o[a] < (float)p.dims[a])) miss = true;
         continue;
       }
-      const int Pe = r.d[a] > 0.f ? 0 : p.dims[a];
-      const Event Ea{a, Pe, tplane(Pe, r.o[a], r.inv[a])};
-      if (cmp_ee(r, Ea, E) > 0) E = Ea;
+      const int Pe = d[a] > 0.f ? 0 : p.dims[a];
+      const float ta = tplane(Pe, o[a], inv[a]);
+      if (cmp_events(o, d, a, Pe, ta, ea, eP, te) > 0) {
+        ea = a;
+        eP = Pe;
+        te = ta;
+      }
     }
     if (miss) return false;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (!((moving >> a) & 1)) continue;
-      const int Px = r.d[a] > 0.f ? p.dims[a] : 0;
-      if (cmp_ep(r, E, a, Px) >= 0) miss = true;  // entered at / after the exit of slab a
+      const int Px = d[a] > 0.f ? p.dims[a] : 0;
+      // entered at / after the exit of slab a
+      if (cmp_events(o, d, ea, eP, te, a, Px, tplane(Px, o[a], inv[a])) >= 0) miss = true;
     }
-    if (miss || (tmax_finite && cmp_es(r, E, r.tmax) >= 0)) return false;
+    if (miss || (tmax_finite && cmp_events(o, d, ea, eP, te, TMIN_AXIS, 0, tmax) >= 0)) return false;
+    eaxis = ea;
+    et = te;
+    // the cell entered through the entry plane is exact; the other moving axes are located
+    // (their slow path reads the event plane back from V[eaxis], so that one is set first)
 #pragma unroll
     for (int b = 0; b < 3; ++b)
-      V[b] = ((moving >> b) & 1) ? locate(r, E, b, 0, p.dims[b] - 1) : (int)floorf(r.o[b]);
+      if (b == ea) V[b] = d[b] > 0.f ? 0 : p.dims[b] - 1;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      if (b == ea) continue;
+      V[b] = ((moving >> b) & 1) ? locate(b, 0, p.dims[b] - 1) : (int)floorf(o[b]);
+    }
     ct.add(VF_CTR_LOCATES, 3);
-    set_tier(p, 0);
+    set_tier(s_tw, 0);
     N = p.root;
-    hd = load_header<KINDS>(buf, kind, N, ct);
+    hd = load_header<KINDS>(buf, tw & 3u, N, ct);
     stale = 0;
     stale_lc = 0;
     return true;
@@ -430,12 +413,11 @@ struct Lane {
   // Invariant: V >> lc is the current (untested) cell of node N at tier t, entered at E.
   // A pop always follows a step, so it lands on a new cell.
   __device__ __forceinline__ int iterate(const TraceParams& p, const uint32_t* __restrict__ buf,
-                                         uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
-#if VF_DESCEND_LOOP
-   for (;;) {
-#endif
+                                         const uint32_t* s_tw, uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
     int nt = t;       // tier after this iteration
     uint32_t nN = N;  // node after this iteration
+    const uint32_t kind = tw & 3u;
+    const bool finest = tw & TW_FINEST;
     {
       // -- test the current cell of the current node (ordered_hit_children, one child)
       const uint32_t lx = ((uint32_t)V[0] >> lc) & msk, ly = ((uint32_t)V[1] >> lc) & msk,
@@ -446,7 +428,7 @@ struct Lane {
       if (has_kind<KINDS>(K_RAW) && kind == K_RAW) {
         // 64-bit index: a single-level R(11^3) grid has 2^33 cells (reading A15)
         const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
-        if (!df) {
+        if (!(tw & TW_DF)) {
           child = __ldg(buf + (size_t)N + lin);
           occ = child != 0u;
           ct.add(VF_CTR_RAW_CELLS);
@@ -469,15 +451,11 @@ struct Lane {
         occ = (hd.mask >> lin) & 1u;
         if (occ && !finest) {
           const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
+          const bool last = tw & TW_LAST;
           if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
             child = hd.base + 2u * rank;
           } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-#if VF_SVDAG_WIDE
-            const uint32_t i = hd.k + 1u + rank;
-            child = i < 8u ? sel8(hd.a, hd.b, i) : __ldg(buf + hd.base + 1u + rank);
-#else
             child = __ldg(buf + hd.base + 1u + rank);
-#endif
             ct.add(VF_CTR_SVDAG_PTRS);
             ct.add(VF_CTR_FORMAT_BYTES, 4);
           } else {
@@ -495,105 +473,87 @@ struct Lane {
         // descend at event E. The child cell needs V's bits >= lc(t+1); if some of those are
         // stale (the ray moved inside a cell of size 2^stale_lc since they were exact), derive the
         // exact finest voxel of the stale axes within the current cell (bits >= lc are exact).
-        if (stale && lc - field4(p.lf_pack, t + 1) < stale_lc) {
+        if (stale && twf(tw, TW_LCN, 4) < stale_lc) {
 #pragma unroll
           for (int b = 0; b < 3; ++b)
             if ((stale >> b) & 1) {
               const int lo = (V[b] >> lc) << lc;
-              V[b] = locate(r, E, b, lo, lo + (1 << lc) - 1);
+              V[b] = locate(b, lo, lo + (1 << lc) - 1);
               ct.add(VF_CTR_LOCATES);
             }
           stale = 0;
           stale_lc = 0;
         }
-        if (!RESTART || ((p.top_mask >> t) & 1u)) stk[t] = N;
+        if (!RESTART || (tw & TW_TOP)) stk[t] = N;
         nt = t + 1;
         nN = child;
         ct.add(VF_CTR_DESCENTS);
       }
     }
-    if (nt == t) step(p, buf, stk, ct, nt, nN);
-    if (nt < 0) return IT_MISS;
+    if (nt == t) {
+      step(p, stk, ct, nt, nN);
+      if (nt < 0) return IT_MISS;
+    }
     // tier change (descent or pop), shared by both paths so a warp mixing them runs it once
     if (nt != t) {
-#if VF_DESCEND_LOOP
-      const bool descended = nt > t;
-#endif
-      set_tier(p, nt);
+      set_tier(s_tw, nt);
       N = nN;
-      hd = load_header<KINDS>(buf, kind, N, ct);
-#if VF_DESCEND_LOOP
-      if (descended) continue;  // test the child's cell in the same iteration: one step per call
-#endif
+      hd = load_header<KINDS>(buf, tw & 3u, N, ct);
     }
     return IT_CONTINUE;
-#if VF_DESCEND_LOOP
-   }
-#endif
   }
 
   // -- step: exact next event among the three axes at this tier's cell size. Sets nt < 0 when
   // the segment ends (miss), nt < t (with nN) when the step leaves the current node.
-  __device__ __forceinline__ void step(const TraceParams& p, const uint32_t* __restrict__ buf,
-                                       uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct, int& nt, uint32_t& nN) {
+  __device__ __forceinline__ void step(const TraceParams& p, uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct, int& nt,
+                                       uint32_t& nN) {
     ct.add(VF_CTR_STEPS);
     int Pn[3];
     float tn[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const int c = V[a] >> lc;
-      Pn[a] = (((dneg >> a) & 1) ? c : c + 1) << lc;
-      tn[a] = ((moving >> a) & 1) ? tplane(Pn[a], r.o[a], r.inv[a]) : __int_as_float(0x7f800000);
+      // next plane on axis a at this tier's cell size (inv = +inf makes a d = 0 axis never step)
+      Pn[a] = ((V[a] >> lc) + 1 - ((dneg >> a) & 1)) << lc;
+      tn[a] = tplane(Pn[a], o[a], inv[a]);
     }
     const float m = fminf(fminf(tn[0], tn[1]), tn[2]);
     const float thr = fmaf(m, kCertEps, m);
     const int c = (tn[0] <= thr ? 1 : 0) | (tn[1] <= thr ? 2 : 0) | (tn[2] <= thr ? 4 : 0);
-    int S, a0;
+    int S;
     if ((c & (c - 1)) == 0) {
+      // one candidate: it is the fp32 minimum, and certified to be the exact one
       S = c;
-      a0 = __ffs(c) - 1;
+      eaxis = c >> 1;
+      et = m;
     } else {
-      const int res = argmin_exact(r.o[0], r.o[1], r.o[2], r.d[0], r.d[1], r.d[2], Pn[0], Pn[1], Pn[2], tn[0], tn[1],
-                                   tn[2], c);
+      const int res = argmin_exact(o[0], o[1], o[2], d[0], d[1], d[2], Pn[0], Pn[1], Pn[2], tn[0], tn[1], tn[2], c);
       S = res & 7;
-      a0 = res >> 4;
+      eaxis = res >> 4;
+      et = sel3(tn, eaxis);
       ct.add(VF_CTR_NEAR_TIES);
     }
-    E.axis = a0;
-    E.P = sel3(Pn, a0);
-    E.t = sel3(tn, a0);
-    if (tmax_finite && cmp_es(r, E, r.tmax) >= 0) {  // segment ends (reading A7)
+    // every axis of S steps into the cell adjacent to its plane (exact ties together, reading A2)
+    int x = 0;
+    bool out_of_box = false;
+    int nV[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const bool s = (S >> a) & 1;
+      const int nv = Pn[a] - ((dneg >> a) & 1);
+      out_of_box |= s && (uint32_t)nv >= (uint32_t)p.dims[a];
+      x |= s ? (nv ^ V[a]) : 0;
+      nV[a] = s ? nv : V[a];
+    }
+    if (out_of_box) {  // left the root box
       nt = -1;
       return;
     }
-    uint32_t h;
-    if (S == (1 << a0)) {
-      // common case: one axis steps into the cell adjacent to plane E.P
-      const int nv = E.P - ((dneg >> a0) & 1);
-      if ((uint32_t)nv >= (uint32_t)sel3(p.dims, a0)) {  // left the root box
-        nt = -1;
-        return;
-      }
-      h = 31u - __clz((uint32_t)(nv ^ sel3(V, a0)));
-      V[0] = a0 == 0 ? nv : V[0];
-      V[1] = a0 == 1 ? nv : V[1];
-      V[2] = a0 == 2 ? nv : V[2];
-    } else {
-      // exact tie: every axis of S steps at once (reading A2)
-      h = 0;
-      bool out_of_box = false;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        if (!((S >> a) & 1)) continue;
-        const int nv = Pn[a] - ((dneg >> a) & 1);
-        if (nv < 0 || nv >= p.dims[a]) out_of_box = true;
-        h = max(h, 31u - __clz((uint32_t)(nv ^ V[a])));
-        V[a] = nv;
-      }
-      if (out_of_box) {  // left the root box
-        nt = -1;
-        return;
-      }
+    for (int a = 0; a < 3; ++a) V[a] = nV[a];
+    // the segment ends at tmax (reading A7); E is read back through V[eaxis], so after the update
+    if (tmax_finite && cmp_es(tmax) >= 0) {
+      nt = -1;
+      return;
     }
     if (lc) {
       stale |= ~S & moving;
@@ -601,8 +561,11 @@ struct Lane {
     }
     stale &= ~S;
     budget -= __popc(S);  // L1 distance moved (DF tiers only use it)
-    const int tau = (int)field4(p.tau_pack, h);
-    if (tau < t) {
+    // h = highest bit in which the old and new cells differ; the step leaves this tier's node iff
+    // h >= lc(t-1) (the node's edge), and then tau(h) is the deepest tier whose node holds both
+    const uint32_t h = 31u - __clz((uint32_t)x);
+    if (h >= twf(tw, TW_LCP, 4)) {
+      const int tau = (int)field4(p.tau_pack, h);
       ct.add(VF_CTR_POPS);
       // left the current node: pop (stack) or restart from the level root
       // (restart: from the top of tau's level — the following iterations re-descend through the
@@ -613,7 +576,7 @@ struct Lane {
     }
   }
 
-  __device__ __forceinline__ int4 hit_record() const { return make_int4(V[0], V[1], V[2], __float_as_int(E.t)); }
+  __device__ __forceinline__ int4 hit_record() const { return make_int4(V[0], V[1], V[2], __float_as_int(et)); }
 
   // Closest-hit payload (the paper's closest-hit shader): the hit
   // voxel's terminating integer (its RGBA) and the entry-face normal -sign(d_a) e_a of the
@@ -622,10 +585,11 @@ struct Lane {
   __device__ __forceinline__ uint2 payload_record(const uint32_t* __restrict__ buf) const {
     const uint32_t lx = ((uint32_t)V[0] >> lc) & msk, ly = ((uint32_t)V[1] >> lc) & msk,
                    lz = ((uint32_t)V[2] >> lc) & msk;
+    const uint32_t kind = tw & 3u;
     uint32_t rgba = 0;
     if (kind == K_RAW) {
       const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
-      rgba = __ldg(buf + (size_t)N + lin * (df ? 2u : 1u));
+      rgba = __ldg(buf + (size_t)N + lin * ((tw & TW_DF) ? 2u : 1u));
     } else {
       const uint32_t lin = lx + (ly << sx) + (lz << sxy);
       const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
@@ -637,17 +601,17 @@ struct Lane {
         rgba = __ldg(buf + hd.base + rank);
     }
     uint32_t nrm = 0;
-    if (E.axis != TMIN_AXIS) {
+    if (eaxis != TMIN_AXIS) {
       // every axis whose voxel-slab entry plane is crossed exactly at E entered the cell (a finer
       // plane may coincide with the event of a coarse step): exact comparisons, lowest axis wins
-      int a = E.axis;
+      int a = eaxis;
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
         if (b >= a || !((moving >> b) & 1)) continue;
         const int plane = ((dneg >> b) & 1) ? V[b] + 1 : V[b];
-        if (cmp_ep(r, E, b, plane) == 0) a = b;
+        if (cmp_eq(b, plane) == 0) a = b;
       }
-      const uint32_t v = sel3(r.d, a) > 0.f ? 0xFFu : 0x01u;  // int8 -1 or +1
+      const uint32_t v = sel3(d, a) > 0.f ? 0xFFu : 0x01u;  // int8 -1 or +1
       nrm = v << (8 * a);
     }
     return make_uint2(rgba, nrm);
@@ -655,6 +619,12 @@ struct Lane {
 };
 
 __device__ __forceinline__ int4 miss_record() { return make_int4(-1, -1, -1, 0x7f800000); }
+
+// Stage the tier words in shared memory (one LDS per tier change instead of field extraction).
+__device__ __forceinline__ void stage_tiers(const TraceParams& p, uint32_t* s_tw) {
+  if (threadIdx.x < VF_MAX_TIERS) s_tw[threadIdx.x] = p.tword[threadIdx.x];
+  __syncthreads();
+}
 
 // One thread per ray, 128-thread blocks.
 #ifndef VF_MINB
@@ -666,16 +636,18 @@ __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const Tra
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
                                                     uint64_t n, unsigned long long* __restrict__ counters,
                                                     unsigned long long* __restrict__ work) {
+  __shared__ uint32_t s_tw[VF_MAX_TIERS];
+  stage_tiers(p, s_tw);
   const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   Ctr<COUNT> ct;
   if (gid < n) {
     Lane<KINDS, RESTART, COUNT> L;
     uint32_t stk[VF_MAX_TIERS];
     int4 out = miss_record();
-    if (L.start(p, buf, __ldg(rays + 2 * gid), __ldg(rays + 2 * gid + 1), ct)) {
+    if (L.start(p, buf, s_tw, __ldg(rays + 2 * gid), __ldg(rays + 2 * gid + 1), ct)) {
       int res;
       do {
-        res = L.iterate(p, buf, stk, ct);
+        res = L.iterate(p, buf, s_tw, stk, ct);
       } while (res == IT_CONTINUE);
       if (res == IT_HIT) {
         out = L.hit_record();
@@ -703,6 +675,8 @@ __global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceP
                                                                    int4* __restrict__ hits, uint64_t n,
                                                                    unsigned long long* __restrict__ counters,
                                                                    unsigned long long* __restrict__ work) {
+  __shared__ uint32_t s_tw[VF_MAX_TIERS];
+  stage_tiers(p, s_tw);
   Ctr<COUNT> ct;
   Lane<KINDS, RESTART, COUNT> L;
   uint32_t stk[VF_MAX_TIERS];
@@ -722,7 +696,7 @@ __global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceP
         idx = base + __popc(idle & lt);
         if (idx < n) {
           ct.add(VF_CTR_RAYS);
-          if (L.start(p, buf, __ldg(rays + 2 * idx), __ldg(rays + 2 * idx + 1), ct))
+          if (L.start(p, buf, s_tw, __ldg(rays + 2 * idx), __ldg(rays + 2 * idx + 1), ct))
             active = true;
           else {
             hits[idx] = miss_record();
@@ -737,7 +711,7 @@ __global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceP
       continue;
     }
     if (active) {
-      const int res = L.iterate(p, buf, stk, ct);
+      const int res = L.iterate(p, buf, s_tw, stk, ct);
       if (res != IT_CONTINUE) {
         if (res == IT_HIT) ct.add(VF_CTR_HITS);
         hits[idx] = res == IT_HIT ? L.hit_record() : miss_record();

@@ -62,6 +62,24 @@ struct TraceParams {
   uint32_t root;        // word 0 (root pointer); 0 => empty volume
   uint32_t level_top_pack_lo;  // 4 bits per tier: tier index of its level's top (tiers 0..7)
   uint32_t level_top_pack_hi;  // tiers 8..15
+  // One packed word per tier, staged in shared memory by the trace kernels and read once per tier
+  // change (TW_* below): everything the traversal needs about the current tier.
+  uint32_t tword[VF_MAX_TIERS];
+};
+
+// Tier-word fields (TraceParams::tword).
+enum : uint32_t {
+  TW_KIND = 0,      // 2 bits: TierKind
+  TW_LC = 2,        // 4 bits: lc(t), log2 cell edge in voxels
+  TW_LCN = 6,       // 4 bits: lc(t+1) (0 at the finest tier)
+  TW_LCP = 10,      // 4 bits: lc(t-1), the edge of tier t's node; 15 at tier 0 (never left)
+  TW_SX = 14,       // 4 bits: shift of the y cell index in the linear cell index
+  TW_SXY = 18,      // 5 bits: shift of the z cell index
+  TW_MB = 23,       // 4 bits: width of a per-axis cell index (lf; 12 at tier 0)
+  TW_LAST = 1u << 27,    // last tier of its level: cells are terminating integers
+  TW_FINEST = 1u << 28,  // last tier overall: cells are voxels
+  TW_DF = 1u << 29,      // DF grid: 2-word cells {TermInt, L1 distance}
+  TW_TOP = 1u << 30,     // first tier of its level
 };
 
 struct Handle {
