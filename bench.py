@@ -218,12 +218,20 @@ def run_ours(args):
 
     incoh = CONFIGS[cfg][1] == "incoherent"  # VF_TRACE_INCOHERENT hint for secondary-style rays
 
-    def step():
-        handle.trace(rays, hits, restart=args.restart, incoherent=incoh)
+    # N > 1: the frame's trace and its hit gather are pipelined over K row chunks of the rank's
+    # (padded) hit buffer — chunk k's NCCL gather overlaps the trace of chunk k+1.
+    pipe = shard.ChunkedGather(counts, args.gather_chunks, dev) if world > 1 else None
+    if pipe is not None:
+        hits = pipe.hits
 
-    def gather():  # the one collective: hit buffers to rank 0 (NCCL)
-        if world > 1:
-            shard.gather_hits(hits, counts)
+    def step():
+        if pipe is None:
+            handle.trace(rays, hits, restart=args.restart, incoherent=incoh)
+        else:
+            pipe.run(lambda lo, hi, hv: handle.trace(rays[lo:hi], hv, restart=args.restart, incoherent=incoh))
+
+    def gather():  # (N > 1: inside step(), chunk by chunk)
+        pass
 
     for _ in range(args.warmup):
         step()
@@ -316,7 +324,7 @@ def run_ours(args):
                 "note": "pointer-chasing; latency/issue-bound, see profiles/"}
 
         # ---- CPU baseline (oracle) on a bounded sample + parity of the sample
-        hits_np = hits.cpu().numpy()
+        hits_np = hits[:n_local].cpu().numpy()
         gxyz, gt = hits_np[:, :3], hits_np[:, 3].view(np.float32)
         cpu, ref_idx, ref = None, None, None
         sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -340,7 +348,7 @@ def run_ours(args):
                        "parallelism": f"ray tiles 16x16 interleaved over {world} GPU(s); volume replicated"},
             "e2e": {"value": round(e2e_val, 2), "unit": "Mrays/s", "h2d_bytes_per_step": n_local * 32,
                     "d2h_bytes_per_step": n_local * 16},
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * (len(pipe.bounds) if pipe is not None else 1),
             "roofline": roof,
             "issue_roofline": issue,
             "cpu_baseline": cpu,
@@ -483,6 +491,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-format sweep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--gather-chunks", type=int, default=4, help="N>1: trace/gather pipeline depth")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -47,6 +47,52 @@ def gather_hits(hits, counts, group=None, dst: int = 0):
     return None
 
 
+def chunk_bounds(counts, k: int):
+    """Row ranges [lo, hi) of the K gather chunks over the padded (max(counts), 4) hit buffer; the
+    same on every rank, so every chunk is one equal-sized collective (SURVEY.md §8(e) Overlap)."""
+    m = max(counts)
+    k = max(1, min(k, m))
+    return [(i * m // k, (i + 1) * m // k) for i in range(k)]
+
+
+class ChunkedGather:
+    """Trace-and-gather pipeline of one frame (SURVEY.md §8(e) "Overlap"): the rank's hit buffer is
+    padded to max(counts) rows and cut into K row chunks; after chunk k is traced, its gather to
+    `dst` is enqueued asynchronously (the NCCL stream waits only for the work issued so far), so
+    chunk k's transfer overlaps the trace of chunk k+1. Still exactly one kind of collective: a
+    gather of hit records to rank 0."""
+
+    def __init__(self, counts, k: int, device, group=None, dst: int = 0):
+        import torch
+        import torch.distributed as dist
+        self.counts, self.group, self.dst = counts, group, dst
+        self.rank = dist.get_rank(group)
+        self.m = max(counts)
+        self.bounds = chunk_bounds(counts, k)
+        self.hits = torch.empty((self.m, 4), dtype=torch.int32, device=device)
+        self.recv = ([torch.empty((self.m, 4), dtype=torch.int32, device=device) for _ in counts]
+                     if self.rank == dst else None)
+
+    def run(self, trace_chunk):
+        """trace_chunk(lo, hi, hits_view) traces local rays [lo, hi) into hits_view; rows beyond the
+        rank's count are padding. Returns the list of per-rank hit buffers on dst, None elsewhere."""
+        import torch.distributed as dist
+        n_local = self.counts[self.rank]
+        works = []
+        for lo, hi in self.bounds:
+            hl = min(hi, n_local)
+            if hl > lo:
+                trace_chunk(lo, hl, self.hits[lo:hl])
+            gl = [b[lo:hi] for b in self.recv] if self.recv is not None else None
+            works.append(dist.gather(self.hits[lo:hi], gather_list=gl, dst=self.dst, group=self.group,
+                                     async_op=True))
+        for w in works:
+            w.wait()
+        if self.recv is None:
+            return None
+        return [b[:c] for b, c in zip(self.recv, self.counts)]
+
+
 def assemble(bufs, perm: np.ndarray, width: int, world: int, tile: int = TILE) -> np.ndarray:
     """Un-permute gathered per-rank hits into a row-major (n_pixels, 4) image buffer."""
     n = len(perm)

@@ -76,3 +76,61 @@ def test_tile_order_is_a_permutation_with_warp_tiles():
     # the first 32 rays form one 8x4 warp tile
     px, py = perm[:32] % 64, perm[:32] // 64
     assert px.max() - px.min() == 7 and py.max() - py.min() == 3
+
+
+def _worker_chunked(rank, world, port, width, height, k, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2410_14128_b200 import shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    perm = R.tile_order(width, height)
+    own = shard.shard(perm, width, rank, world)
+    pix = torch.from_numpy(perm[own].astype(np.int32))
+    counts = shard.shard_counts(perm, width, world)
+    pipe = shard.ChunkedGather(counts, k, "cpu")
+    seen = []
+
+    def trace_chunk(lo, hi, hv):  # stand-in for vf_trace on local rays [lo, hi)
+        seen.append((lo, hi))
+        p = pix[lo:hi]
+        hv.copy_(torch.stack([p, p * 3, -p, p % 7], 1))
+
+    bufs = pipe.run(trace_chunk)
+    # the chunks cover exactly the rank's own rays, in order
+    assert seen[0][0] == 0 and seen[-1][1] == counts[rank]
+    assert all(a[1] == b[0] for a, b in zip(seen, seen[1:]))
+    if rank == 0:
+        q.put(shard.assemble(bufs, perm, width, world))
+    dist.destroy_process_group()
+
+
+def test_chunked_trace_gather_pipeline_gloo():
+    """SURVEY §8(e) Overlap: the trace/gather pipeline over K row chunks of the padded hit buffers
+    reassembles the same frame as one gather (ragged shards, K not dividing the rows)."""
+    width, height, world, k = 72, 40, 2, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_chunked, args=(r, world, port, width, height, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    img = q.get(timeout=120)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    pix = np.arange(width * height)
+    np.testing.assert_array_equal(img[:, 0], pix)
+    np.testing.assert_array_equal(img[:, 1], pix * 3)
+    np.testing.assert_array_equal(img[:, 2], -pix)
+    np.testing.assert_array_equal(img[:, 3], pix % 7)
+
+
+def test_chunk_bounds_cover_padded_rows():
+    from paper_2410_14128_b200 import shard
+    for counts, k in (([10, 7], 3), ([5], 8), ([1000, 999, 998], 4)):
+        b = shard.chunk_bounds(counts, k)
+        assert b[0][0] == 0 and b[-1][1] == max(counts)
+        assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
+        assert all(hi > lo for lo, hi in b)
