@@ -37,6 +37,7 @@
 #include <stdlib.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "vf_internal.cuh"
 
@@ -164,10 +165,19 @@ __device__ __forceinline__ bool has_kind(uint32_t k) {
 
 __device__ __forceinline__ uint32_t twf(uint32_t w, uint32_t pos, uint32_t len) { return (w >> pos) & ((1u << len) - 1u); }
 
-// Node header registers for the current tier.
+// Node header registers for the current tier. The occupancy mask is 64-bit only when an N^3-tree
+// tier is present (SVO / SVDAG masks are 8-bit: one POPC instead of two on the hot path).
+template <uint32_t KINDS>
 struct Header {
-  uint64_t mask;  // SVO/SVDAG: valid bits; N^3: 64-bit occupancy
-  uint32_t base;  // SVO: first child; SVDAG: node address; N^3: children block
+  using Mask = typename std::conditional<((KINDS >> K_NTREE) & 1u) != 0, uint64_t, uint32_t>::type;
+  Mask mask;      // SVO/SVDAG: valid bits; N^3: 64-bit occupancy
+  uint32_t base;  // SVO: first child; N^3: children block (SVDAG: the node address is N)
+  __device__ __forceinline__ uint32_t rank(uint32_t lin) const {
+    if constexpr (sizeof(Mask) == 8)
+      return __popcll(mask & ((1ull << lin) - 1ull));
+    else
+      return __popc(mask & ((1u << lin) - 1u));
+  }
 };
 
 // Per-ray work counters of the VF_COUNTERS variant (SURVEY.md §8(d) "Counts come from a
@@ -197,12 +207,10 @@ struct Ctr {
   }
 };
 
+// Read the header of node N of a tier of the given kind into h (a Raw tier has none).
 template <uint32_t KINDS, bool COUNT>
-__device__ __forceinline__ Header load_header(const uint32_t* __restrict__ buf, uint32_t kind, uint32_t N,
-                                              Ctr<COUNT>& ct) {
-  Header h;
-  h.mask = 0;
-  h.base = N;
+__device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, uint32_t kind, uint32_t N,
+                                            Header<KINDS>& h, Ctr<COUNT>& ct) {
   if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
     const uint2 v = __ldg(reinterpret_cast<const uint2*>(buf + N));
     h.base = v.x;
@@ -215,12 +223,11 @@ __device__ __forceinline__ Header load_header(const uint32_t* __restrict__ buf, 
     ct.add(VF_CTR_FORMAT_BYTES, 4);
   } else if (has_kind<KINDS>(K_NTREE) && kind == K_NTREE) {
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(buf + N));
-    h.mask = (uint64_t)v.x | ((uint64_t)v.y << 32);
+    h.mask = (typename Header<KINDS>::Mask)((uint64_t)v.x | ((uint64_t)v.y << 32));
     h.base = v.z;
     ct.add(VF_CTR_NTREE_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 16);
   }
-  return h;
 }
 
 enum { IT_CONTINUE = 0, IT_HIT = 1, IT_MISS = 2 };
@@ -245,7 +252,7 @@ struct Lane {
   uint32_t N;     // current node (word address)
   uint32_t tw;    // tier word of tier t
   uint32_t lc, msk, sx, sxy;  // decoded from tw
-  Header hd;
+  Header<KINDS> hd;
   int stale;          // axes whose bits below stale_lc are not exact at E
   uint32_t stale_lc;  // bits of V below this are stale on the axes in `stale`
   int moving;         // axes with d != 0
@@ -404,16 +411,36 @@ struct Lane {
     ct.add(VF_CTR_LOCATES, 3);
     set_tier(s_tw, 0);
     N = p.root;
-    hd = load_header<KINDS>(buf, tw & 3u, N, ct);
+    hd.mask = 0;
+    hd.base = 0;
+    load_header<KINDS>(buf, tw & 3u, N, hd, ct);
     stale = 0;
     stale_lc = 0;
     return true;
   }
 
-  // Invariant: V >> lc is the current (untested) cell of node N at tier t, entered at E.
+  // Invariant: V >> lc is the current (untested) cell of node N at tier t, entered at E, except
+  // right after a descent that needs sub-cell bits which are stale (below).
   // A pop always follows a step, so it lands on a new cell.
   __device__ __forceinline__ int iterate(const TraceParams& p, const uint32_t* __restrict__ buf,
                                          const uint32_t* s_tw, uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
+    // -- first iteration after a descent: this tier's cell needs V's bits >= lc; if some of those
+    // are stale (the ray moved inside a cell of size 2^stale_lc since they were exact), derive the
+    // exact finest voxel of the stale axes within the parent cell (edge 2^lc(t-1), bits above it
+    // exact). Done here rather than in the descent branch so that V is only ever updated in
+    // sequence (this block, then step), never on two converging paths.
+    if (stale && lc < stale_lc) {
+      const uint32_t lcp = twf(tw, TW_LCP, 4);
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if ((stale >> b) & 1) {
+          const int lo = (V[b] >> lcp) << lcp;
+          V[b] = locate(b, lo, lo + (1 << lcp) - 1);
+          ct.add(VF_CTR_LOCATES);
+        }
+      stale = 0;
+      stale_lc = 0;
+    }
     int nt = t;       // tier after this iteration
     uint32_t nN = N;  // node after this iteration
     const uint32_t kind = tw & 3u;
@@ -450,12 +477,12 @@ struct Lane {
         const uint32_t lin = lx + (ly << sx) + (lz << sxy);
         occ = (hd.mask >> lin) & 1u;
         if (occ && !finest) {
-          const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
+          const uint32_t rank = hd.rank(lin);
           const bool last = tw & TW_LAST;
           if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
             child = hd.base + 2u * rank;
           } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-            child = __ldg(buf + hd.base + 1u + rank);
+            child = __ldg(buf + N + 1u + rank);
             ct.add(VF_CTR_SVDAG_PTRS);
             ct.add(VF_CTR_FORMAT_BYTES, 4);
           } else {
@@ -470,20 +497,7 @@ struct Lane {
       }
       if (occ) {
         if (finest) return IT_HIT;  // unit intersection
-        // descend at event E. The child cell needs V's bits >= lc(t+1); if some of those are
-        // stale (the ray moved inside a cell of size 2^stale_lc since they were exact), derive the
-        // exact finest voxel of the stale axes within the current cell (bits >= lc are exact).
-        if (stale && twf(tw, TW_LCN, 4) < stale_lc) {
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-            if ((stale >> b) & 1) {
-              const int lo = (V[b] >> lc) << lc;
-              V[b] = locate(b, lo, lo + (1 << lc) - 1);
-              ct.add(VF_CTR_LOCATES);
-            }
-          stale = 0;
-          stale_lc = 0;
-        }
+        // descend at event E (the child's entry cell is derived at the top of the next iteration)
         if (!RESTART || (tw & TW_TOP)) stk[t] = N;
         nt = t + 1;
         nN = child;
@@ -498,7 +512,7 @@ struct Lane {
     if (nt != t) {
       set_tier(s_tw, nt);
       N = nN;
-      hd = load_header<KINDS>(buf, tw & 3u, N, ct);
+      load_header<KINDS>(buf, tw & 3u, N, hd, ct);
     }
     return IT_CONTINUE;
   }
@@ -532,24 +546,22 @@ struct Lane {
       et = sel3(tn, eaxis);
       ct.add(VF_CTR_NEAR_TIES);
     }
-    // every axis of S steps into the cell adjacent to its plane (exact ties together, reading A2)
+    // every axis of S steps into the cell adjacent to its plane (exact ties together, reading A2);
+    // V is updated in place (on a miss it is not used again)
     int x = 0;
     bool out_of_box = false;
-    int nV[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const bool s = (S >> a) & 1;
       const int nv = Pn[a] - ((dneg >> a) & 1);
       out_of_box |= s && (uint32_t)nv >= (uint32_t)p.dims[a];
       x |= s ? (nv ^ V[a]) : 0;
-      nV[a] = s ? nv : V[a];
+      V[a] = s ? nv : V[a];
     }
     if (out_of_box) {  // left the root box
       nt = -1;
       return;
     }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) V[a] = nV[a];
     // the segment ends at tmax (reading A7); E is read back through V[eaxis], so after the update
     if (tmax_finite && cmp_es(tmax) >= 0) {
       nt = -1;
@@ -592,11 +604,11 @@ struct Lane {
       rgba = __ldg(buf + (size_t)N + lin * ((tw & TW_DF) ? 2u : 1u));
     } else {
       const uint32_t lin = lx + (ly << sx) + (lz << sxy);
-      const uint32_t rank = __popcll(hd.mask & ((1ull << lin) - 1ull));
+      const uint32_t rank = hd.rank(lin);
       if (kind == K_SVO)
         rgba = __ldg(buf + hd.base + 2u * rank);
       else if (kind == K_SVDAG)
-        rgba = __ldg(buf + __ldg(buf + hd.base + 1u + rank));
+        rgba = __ldg(buf + __ldg(buf + N + 1u + rank));
       else
         rgba = __ldg(buf + hd.base + rank);
     }
