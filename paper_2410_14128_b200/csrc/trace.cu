@@ -214,11 +214,11 @@ __device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, ui
   if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
     const uint2 v = __ldg(reinterpret_cast<const uint2*>(buf + N));
     h.base = v.x;
-    h.mask = v.y & 0xFFu;
+    h.mask = v.y;  // valid bits 0-7 (leaf bits 8-15 are never indexed: cell indices are < 8)
     ct.add(VF_CTR_SVO_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 8);
   } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-    h.mask = __ldg(buf + N) & 0xFFu;
+    h.mask = __ldg(buf + N);  // valid bits 0-7 (leaf bits 8-15 never indexed)
     ct.add(VF_CTR_SVDAG_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 4);
   } else if (has_kind<KINDS>(K_NTREE) && kind == K_NTREE) {
@@ -335,13 +335,16 @@ struct Lane {
     return k;
   }
 
+  // s_tw: the tier table staged in shared memory, two uint4 per tier (stage_tiers): one LDS.128
+  // and one LDS.32 per tier change instead of extracting the fields from the tier word.
   __device__ __forceinline__ void set_tier(const uint32_t* s_tw, int nt) {
     t = nt;
-    tw = s_tw[nt];
-    lc = twf(tw, TW_LC, 4);
-    msk = (1u << twf(tw, TW_MB, 4)) - 1u;
-    sx = twf(tw, TW_SX, 4);
-    sxy = twf(tw, TW_SXY, 5);
+    const uint4 a = reinterpret_cast<const uint4*>(s_tw)[2 * nt];
+    tw = a.x;
+    lc = a.y;
+    msk = a.z;
+    sx = a.w;
+    sxy = s_tw[8 * nt + 4];
     budget = 0;
   }
 
@@ -419,28 +422,11 @@ struct Lane {
     return true;
   }
 
-  // Invariant: V >> lc is the current (untested) cell of node N at tier t, entered at E, except
-  // right after a descent that needs sub-cell bits which are stale (below).
+  // Invariant: V >> lc is the current (untested) cell of node N at tier t, entered at E (the
+  // tier-change block below re-derives stale sub-cell bits right after a descent).
   // A pop always follows a step, so it lands on a new cell.
   __device__ __forceinline__ int iterate(const TraceParams& p, const uint32_t* __restrict__ buf,
                                          const uint32_t* s_tw, uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
-    // -- first iteration after a descent: this tier's cell needs V's bits >= lc; if some of those
-    // are stale (the ray moved inside a cell of size 2^stale_lc since they were exact), derive the
-    // exact finest voxel of the stale axes within the parent cell (edge 2^lc(t-1), bits above it
-    // exact). Done here rather than in the descent branch so that V is only ever updated in
-    // sequence (this block, then step), never on two converging paths.
-    if (stale && lc < stale_lc) {
-      const uint32_t lcp = twf(tw, TW_LCP, 4);
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-        if ((stale >> b) & 1) {
-          const int lo = (V[b] >> lcp) << lcp;
-          V[b] = locate(b, lo, lo + (1 << lcp) - 1);
-          ct.add(VF_CTR_LOCATES);
-        }
-      stale = 0;
-      stale_lc = 0;
-    }
     int nt = t;       // tier after this iteration
     uint32_t nN = N;  // node after this iteration
     const uint32_t kind = tw & 3u;
@@ -513,6 +499,23 @@ struct Lane {
       set_tier(s_tw, nt);
       N = nN;
       load_header<KINDS>(buf, tw & 3u, N, hd, ct);
+      // after a descent, the new tier's cell needs V's bits >= lc; if some of those are stale (the
+      // ray moved inside a cell of size 2^stale_lc since they were exact), derive the exact finest
+      // voxel of the stale axes within the parent cell (edge 2^lc(t-1); bits above it exact).
+      // (never true after a pop: a pop lands on a tier with lc >= stale_lc)
+      if (stale && lc < stale_lc) {
+        const uint32_t lcp = twf(tw, TW_LCP, 4);
+        const int st = stale & moving;
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          if ((st >> b) & 1) {
+            const int lo = (V[b] >> lcp) << lcp;
+            V[b] = locate(b, lo, lo + (1 << lcp) - 1);
+            ct.add(VF_CTR_LOCATES);
+          }
+        stale = 0;
+        stale_lc = 0;
+      }
     }
     return IT_CONTINUE;
   }
@@ -532,16 +535,18 @@ struct Lane {
     }
     const float m = fminf(fminf(tn[0], tn[1]), tn[2]);
     const float thr = fmaf(m, kCertEps, m);
-    const int c = (tn[0] <= thr ? 1 : 0) | (tn[1] <= thr ? 2 : 0) | (tn[2] <= thr ? 4 : 0);
-    int S;
-    if ((c & (c - 1)) == 0) {
-      // one candidate: it is the fp32 minimum, and certified to be the exact one
-      S = c;
-      eaxis = c >> 1;
+    // s[a]: axis a steps. One candidate within the certification margin of the fp32 minimum is
+    // certified to be the exact minimum; several go to the exact argmin (ties step together).
+    bool s[3] = {tn[0] <= thr, tn[1] <= thr, tn[2] <= thr};
+    int S = (s[0] ? 1 : 0) | (s[1] ? 2 : 0) | (s[2] ? 4 : 0);
+    if ((S & (S - 1)) == 0) {
+      eaxis = s[0] ? 0 : (s[1] ? 1 : 2);
       et = m;
     } else {
-      const int res = argmin_exact(o[0], o[1], o[2], d[0], d[1], d[2], Pn[0], Pn[1], Pn[2], tn[0], tn[1], tn[2], c);
+      const int res = argmin_exact(o[0], o[1], o[2], d[0], d[1], d[2], Pn[0], Pn[1], Pn[2], tn[0], tn[1], tn[2], S);
       S = res & 7;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) s[a] = (res >> a) & 1;
       eaxis = res >> 4;
       et = sel3(tn, eaxis);
       ct.add(VF_CTR_NEAR_TIES);
@@ -552,11 +557,10 @@ struct Lane {
     bool out_of_box = false;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const bool s = (S >> a) & 1;
       const int nv = Pn[a] - ((dneg >> a) & 1);
-      out_of_box |= s && (uint32_t)nv >= (uint32_t)p.dims[a];
-      x |= s ? (nv ^ V[a]) : 0;
-      V[a] = s ? nv : V[a];
+      out_of_box |= s[a] && (uint32_t)nv >= (uint32_t)p.dims[a];
+      x |= s[a] ? (nv ^ V[a]) : 0;
+      V[a] = s[a] ? nv : V[a];
     }
     if (out_of_box) {  // left the root box
       nt = -1;
@@ -567,8 +571,9 @@ struct Lane {
       nt = -1;
       return;
     }
+    // (axes with d = 0 may be marked too: they never move, and the locate block skips them)
     if (lc) {
-      stale |= ~S & moving;
+      stale |= ~S & 7;
       stale_lc = max(stale_lc, lc);
     }
     stale &= ~S;
@@ -632,9 +637,15 @@ struct Lane {
 
 __device__ __forceinline__ int4 miss_record() { return make_int4(-1, -1, -1, 0x7f800000); }
 
-// Stage the tier words in shared memory (one LDS per tier change instead of field extraction).
+// Stage the tier table in shared memory: per tier {tier word, lc, cell-index mask, y shift} and
+// {z shift} (two uint4), so a tier change is one LDS.128 + one LDS.32 (no field extraction).
 __device__ __forceinline__ void stage_tiers(const TraceParams& p, uint32_t* s_tw) {
-  if (threadIdx.x < VF_MAX_TIERS) s_tw[threadIdx.x] = p.tword[threadIdx.x];
+  if (threadIdx.x < VF_MAX_TIERS) {
+    const uint32_t w = p.tword[threadIdx.x];
+    reinterpret_cast<uint4*>(s_tw)[2 * threadIdx.x] =
+        make_uint4(w, twf(w, TW_LC, 4), (1u << twf(w, TW_MB, 4)) - 1u, twf(w, TW_SX, 4));
+    reinterpret_cast<uint4*>(s_tw)[2 * threadIdx.x + 1] = make_uint4(twf(w, TW_SXY, 5), 0u, 0u, 0u);
+  }
   __syncthreads();
 }
 
@@ -648,7 +659,7 @@ __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const Tra
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
                                                     uint64_t n, unsigned long long* __restrict__ counters,
                                                     unsigned long long* __restrict__ work) {
-  __shared__ uint32_t s_tw[VF_MAX_TIERS];
+  __shared__ __align__(16) uint32_t s_tw[8 * VF_MAX_TIERS];
   stage_tiers(p, s_tw);
   const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   Ctr<COUNT> ct;
@@ -687,7 +698,7 @@ __global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceP
                                                                    int4* __restrict__ hits, uint64_t n,
                                                                    unsigned long long* __restrict__ counters,
                                                                    unsigned long long* __restrict__ work) {
-  __shared__ uint32_t s_tw[VF_MAX_TIERS];
+  __shared__ __align__(16) uint32_t s_tw[8 * VF_MAX_TIERS];
   stage_tiers(p, s_tw);
   Ctr<COUNT> ct;
   Lane<KINDS, RESTART, COUNT> L;
@@ -816,6 +827,9 @@ KernelFn get_kernel(bool restart, bool count, bool persistent) {
 }
 
 KernelFn select_kernel(uint32_t kinds, bool restart, bool count, bool persistent) {
+#ifdef VF_ONLY_KINDS  // fast A/B variant builds (tools/build_variant.sh -DVF_ONLY_KINDS=5): one kind set
+  return kinds == VF_ONLY_KINDS ? get_kernel<VF_ONLY_KINDS>(restart, count, persistent) : nullptr;
+#else
   switch (kinds) {
 #define VF_CASE(k) \
   case k: return get_kernel<k>(restart, count, persistent);
@@ -824,6 +838,7 @@ KernelFn select_kernel(uint32_t kinds, bool restart, bool count, bool persistent
 #undef VF_CASE
     default: return nullptr;
   }
+#endif
 }
 
 // resident blocks per SM for a persistent kernel (cached per function and device)

@@ -1,14 +1,14 @@
 #!/bin/bash
 # Build an A/B variant of libvf.so with extra nvcc defines: tools/build_variant.sh NAME -DFOO=1 ...
+# Only trace.cu is recompiled; the other objects come from the in-tree build (paper_2410_14128_b200/build).
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
 out=build/variant_$name
 mkdir -p $out
-for f in format build trace capi; do
-  nvcc -O3 -std=c++17 --extended-lambda -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
-    -Xcompiler -fvisibility=hidden -I include "$@" -c paper_2410_14128_b200/csrc/$f.cu -o $out/$f.o &
-done
-wait
-nvcc -shared -gencode arch=compute_100a,code=sm_100a -o $out/libvf.so $out/*.o
+[ -f paper_2410_14128_b200/build/capi.o ] || python -c "from paper_2410_14128_b200 import _build; _build.build()" > /dev/null
+nvcc -O3 -std=c++17 --extended-lambda -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
+  -Xcompiler -fvisibility=hidden -I include "$@" -c ${TRACE_SRC:-paper_2410_14128_b200/csrc/trace.cu} -o $out/trace.o
+nvcc -shared -gencode arch=compute_100a,code=sm_100a -o $out/libvf.so $out/trace.o \
+  paper_2410_14128_b200/build/{format,build,capi}.o
 echo $out/libvf.so
