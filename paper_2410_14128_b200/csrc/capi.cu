@@ -1,5 +1,6 @@
 // capi.cu — the extern "C" boundary of libvf.so (include/vf.h). No exception crosses it.
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <new>
@@ -200,25 +201,43 @@ vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hi
   }
   vf_ray* d_rays = (vf_ray*)h->stage;
   vf_hit* d_hits = (vf_hit*)((char*)h->stage + ((rb + 255) & ~(size_t)255));
-  // Pipeline: the frame is cut into chunks that alternate over kPipe internal streams, so the
+  // Pipeline: the frame is cut into chunks; one internal stream copies rays in (copy engine 1),
+  // two trace (alternating, so consecutive chunks' kernels overlap: a small launch lasts as long
+  // as its slowest ray), one copies hits out (copy engine 2), linked per chunk by events — so the
   // host->device copy of chunk i+1, the trace of chunk i and the device->host copy of chunk i-1
-  // overlap (two copy engines + the SMs). Every chunk has its own staging region: no reuse hazard.
+  // overlap with no false dependency between a chunk's copy-out and a later chunk's copy-in.
+  // Every chunk has its own staging region: no reuse hazard. The bound is the PCIe link (rays in:
+  // 32 B/ray); the chunk count trades pipeline fill/drain against per-copy overhead.
   if (!h->pipe[0]) {
     for (int i = 0; i < kPipe; ++i) VF_CUDA_TRY(cudaStreamCreateWithFlags(&h->pipe[i], cudaStreamNonBlocking));
     VF_CUDA_TRY(cudaEventCreateWithFlags(&h->pipe_ev, cudaEventDisableTiming));
+    for (int i = 0; i < 2 * kMaxHostChunks; ++i)
+      VF_CUDA_TRY(cudaEventCreateWithFlags(&h->chunk_ev[i], cudaEventDisableTiming));
   }
   VF_CUDA_TRY(cudaEventRecord(h->pipe_ev, s));  // order after prior work on the caller's stream
-  const uint64_t chunks = n >= (1ull << 18) ? (n >> 17 < 16 ? n >> 17 : 16) : 1;
+  static const uint64_t chunks_env = [] {  // A/B override of the pipeline depth
+    const char* e = getenv("VF_HOST_CHUNKS");
+    const long v = e ? atol(e) : 0;
+    return (uint64_t)(v > 0 && v <= kMaxHostChunks ? v : 0);
+  }();
+  uint64_t chunks = n >= (1ull << 18) ? (n >> 17 < 16 ? n >> 17 : 16) : 1;
+  if (chunks_env) chunks = chunks_env < n ? chunks_env : n;
   const uint64_t per = (n + chunks - 1) / chunks;
+  cudaStream_t cin = h->pipe[0], cout = h->pipe[1];
+  for (int i = 0; i < kPipe; ++i) VF_CUDA_TRY(cudaStreamWaitEvent(h->pipe[i], h->pipe_ev, 0));
   for (uint64_t c = 0; c < chunks; ++c) {
-    cudaStream_t cs = h->pipe[c % kPipe];
-    if (c < (uint64_t)kPipe) VF_CUDA_TRY(cudaStreamWaitEvent(cs, h->pipe_ev, 0));
     const uint64_t b = c * per, m = (b + per <= n) ? per : n - b;
     if (!m) break;
-    VF_CUDA_TRY(cudaMemcpyAsync(d_rays + b, host_rays + b, m * sizeof(vf_ray), cudaMemcpyHostToDevice, cs));
-    vf_status st = launch_trace(h, d_rays + b, m, d_hits + b, trace_flags, cs);
+    cudaEvent_t in_done = h->chunk_ev[2 * c], tr_done = h->chunk_ev[2 * c + 1];
+    cudaStream_t ctr = h->pipe[2 + (c & 1)];
+    VF_CUDA_TRY(cudaMemcpyAsync(d_rays + b, host_rays + b, m * sizeof(vf_ray), cudaMemcpyHostToDevice, cin));
+    VF_CUDA_TRY(cudaEventRecord(in_done, cin));
+    VF_CUDA_TRY(cudaStreamWaitEvent(ctr, in_done, 0));
+    vf_status st = launch_trace(h, d_rays + b, m, d_hits + b, trace_flags, ctr);
     if (st != VF_OK) return st;
-    VF_CUDA_TRY(cudaMemcpyAsync(host_hits + b, d_hits + b, m * sizeof(vf_hit), cudaMemcpyDeviceToHost, cs));
+    VF_CUDA_TRY(cudaEventRecord(tr_done, ctr));
+    VF_CUDA_TRY(cudaStreamWaitEvent(cout, tr_done, 0));
+    VF_CUDA_TRY(cudaMemcpyAsync(host_hits + b, d_hits + b, m * sizeof(vf_hit), cudaMemcpyDeviceToHost, cout));
   }
   for (int i = 0; i < kPipe; ++i) VF_CUDA_TRY(cudaStreamSynchronize(h->pipe[i]));
   return VF_OK;
@@ -286,6 +305,8 @@ void vf_destroy(vf_handle* h) {
   for (int i = 0; i < kPipe; ++i)
     if (h->pipe[i]) cudaStreamDestroy(h->pipe[i]);
   if (h->pipe_ev) cudaEventDestroy(h->pipe_ev);
+  for (int i = 0; i < 2 * kMaxHostChunks; ++i)
+    if (h->chunk_ev[i]) cudaEventDestroy(h->chunk_ev[i]);
   delete h;
 }
 

@@ -92,15 +92,17 @@ struct Handle {
   // staging and pipeline streams for vf_trace_host
   void* stage = nullptr;
   size_t stage_bytes = 0;
-  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t pipe[4] = {nullptr, nullptr, nullptr, nullptr};  // copy-in, copy-out, 2 x trace
   cudaEvent_t pipe_ev = nullptr;
+  cudaEvent_t chunk_ev[2 * 64] = {};  // per chunk: rays copied in, traced (2 * kMaxHostChunks)
   // persistent-trace work counters: kWorkSlots x {next ray, finished blocks}, self-resetting
   unsigned long long* work = nullptr;
   mutable std::atomic<uint32_t> work_slot{0};
 };
 
 constexpr uint32_t kWorkSlots = 64;
-constexpr int kPipe = 3;
+constexpr int kPipe = 4;
+constexpr int kMaxHostChunks = 64;
 // internal trace flag (ablation / tests): persistent warps with dynamic ray refill
 constexpr uint32_t VF_TRACE_PERSISTENT_WARPS = 1u << 30;
 

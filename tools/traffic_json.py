@@ -14,7 +14,7 @@ for r in rows[hi + 1:]:
     if len(r) != len(hdr) or not r[0].isdigit():
         continue
     d = dict(zip(hdr, r))
-    if "trace_kernel" not in d["Kernel Name"]:
+    if "trace_kernel" not in d["Kernel Name"] and "trace_persistent" not in d["Kernel Name"]:
         continue
     v = float(d["Metric Value"].replace(",", ""))
     unit = d["Metric Unit"]
