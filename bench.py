@@ -349,6 +349,9 @@ def run_ours(args):
                 "frac": round(achieved / hbm, 5) if hbm else None, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if hbm else "missing",
                 "algorithmic_bytes_per_ray": round(alg["bytes_per_ray"], 2), "kernel_ms": round(kmean, 4),
+                "sector_bytes_per_ray": round(32 * alg.get("sector_reads", 0) / n_local, 1),
+                "compulsory_bytes_per_ray": round(4 * alg.get("unique_words", 0) / n_local, 2),
+                "compulsory_sector_bytes_per_ray": round(32 * alg.get("unique_sectors", 0) / n_local, 2),
                 "note": "pointer-chasing; latency/issue-bound, see profiles/"}
 
         # ---- CPU baseline (oracle) on a bounded sample + parity of the sample
@@ -453,7 +456,12 @@ def sweep(cfg, vol, rays, hits, stream, flush, args, ref_idx=None, ref=None):
                    "wld_reduction": round(no_wld / st["bytes_used"], 3) if no_wld else None,
                    "roofline_frac": round(alg / (t_ms / 1e3) / 1e9 / hbm, 5) if hbm else None,
                    "cells_per_ray": round(c["cell_tests"] / n, 2), "descents_per_ray": round(c["descents"] / n, 2),
-                   "simt_bound": round(c["cell_tests"] / max(c["warp_max_tests"], 1), 3)}
+                   "simt_bound": round(c["cell_tests"] / max(c["warp_max_tests"], 1), 3),
+                   # sector bytes (32 B x sectors spanned per load) and the frame's
+                   # compulsory format bytes (distinct words read, touch bitmap) per ray
+                   "sector_bytes_per_ray": round(32 * c["sector_reads"] / n, 1),
+                   "compulsory_bytes_per_ray": round(4 * c["unique_words"] / n, 2),
+                   "compulsory_sector_bytes_per_ray": round(32 * c["unique_sectors"] / n, 2)}
             key = f"{cfg}|{h.signature}|{variant}"
             if key in traffic:
                 row["dram_bytes_per_ray"] = round(traffic[key]["dram_bytes_per_launch"] / n, 1)

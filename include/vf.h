@@ -192,7 +192,9 @@ VF_API vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n
  * VF_CTR_FORMAT_BYTES is the algorithmic format traffic: every format word the traversal reads,
  * counted once per read at its load width (Raw cell 4 B, SVO node 8 B, SVDAG mask 4 B + child
  * pointer 4 B, N^3 node 16 B, leaf terminating integer 4 B); ray I/O (48 B/ray) is not included.
- * VF_CTR_EXACT_CALLS counts exact fp64 fallbacks of the certified comparator. */
+ * VF_CTR_EXACT_CALLS counts exact fp64 fallbacks of the certified comparator. The counting run
+ * also keeps a touch bitmap (one bit per format word, n_words / 8 bytes of device memory for the
+ * call) for the distinct words / sectors the frame reads. */
 enum {
   VF_CTR_RAYS = 0,
   VF_CTR_HITS,
@@ -213,6 +215,11 @@ enum {
   VF_CTR_EXACT_CALLS,   /* exact fallbacks (device-global counter) */
   VF_CTR_WARP_MAX_TESTS, /* sum over warps of 32 x (max cell tests of a lane): SIMT bound */
   VF_CTR_DF_SKIPS,      /* DF cells passed without a memory access (distance budget) */
+  VF_CTR_SECTOR_READS,  /* 32-B sectors spanned by the format loads, summed over loads (x 32 B: the
+                           sector-bytes figure of SURVEY.md §8(d); re-reads counted again) */
+  VF_CTR_UNIQUE_WORDS,  /* distinct format words read by the launch (touch bitmap): x 4 B = the
+                           compulsory format bytes of the frame */
+  VF_CTR_UNIQUE_SECTORS, /* distinct 32-B sectors of the format read by the launch */
   VF_NCOUNTERS
 };
 

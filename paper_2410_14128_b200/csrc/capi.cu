@@ -149,11 +149,20 @@ vf_status vf_trace_counters(const vf_handle* h, const vf_ray* rays, uint64_t n, 
   cudaStream_t s = (cudaStream_t)cuda_stream;
   unsigned long long* d = nullptr;
   VF_CUDA_TRY(cudaMalloc(&d, sizeof(unsigned long long) * VF_NCOUNTERS));
+  // touch bitmap: one bit per format word (distinct words / sectors read by the frame)
+  const uint64_t nbw = (h->n_words + 31) / 32;
+  uint32_t* touch = nullptr;
+  if (cudaMalloc(&touch, nbw * sizeof(uint32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    touch = nullptr;  // too large to keep: the distinct-word counters stay 0
+  }
   unsigned long long ex = 0;
   vf_status st = read_exact_calls(&ex, true);
   if (st == VF_OK) {
     cudaMemsetAsync(d, 0, sizeof(unsigned long long) * VF_NCOUNTERS, s);
-    st = launch_trace(h, rays, n, hits, trace_flags, s, d);
+    if (touch) cudaMemsetAsync(touch, 0, nbw * sizeof(uint32_t), s);
+    st = launch_trace(h, rays, n, hits, trace_flags, s, d, nullptr, touch);
+    if (st == VF_OK && touch) st = launch_touch_count(touch, nbw, d, s);
   }
   if (st == VF_OK) {
     unsigned long long hc[VF_NCOUNTERS];
@@ -169,6 +178,7 @@ vf_status vf_trace_counters(const vf_handle* h, const vf_ray* rays, uint64_t n, 
     }
   }
   cudaFree(d);
+  if (touch) cudaFree(touch);
   return st;
 }
 

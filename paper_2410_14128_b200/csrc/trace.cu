@@ -190,8 +190,17 @@ struct Ctr {
 #pragma unroll
       for (int i = 0; i < VF_NCOUNTERS; ++i) v[i] = 0;
   }
+  uint32_t* touch_map = nullptr;  // counting launches: one bit per format word
   __device__ __forceinline__ void add(int i, uint32_t x = 1) {
     if (COUNT) v[i] += x;
+  }
+  // A format load of nw words at word address a: sectors spanned, and the words in the bitmap.
+  __device__ __forceinline__ void touch(size_t a, uint32_t nw) {
+    if constexpr (COUNT) {
+      v[VF_CTR_SECTOR_READS] += (uint32_t)(((a + nw - 1) >> 3) - (a >> 3) + 1);
+      if (touch_map)
+        for (uint32_t i = 0; i < nw; ++i) atomicOr(touch_map + ((a + i) >> 5), 1u << ((a + i) & 31));
+    }
   }
   __device__ __forceinline__ void flush(unsigned long long* out) {
     if constexpr (COUNT) {
@@ -217,16 +226,19 @@ __device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, ui
     h.mask = v.y;  // valid bits 0-7 (leaf bits 8-15 are never indexed: cell indices are < 8)
     ct.add(VF_CTR_SVO_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 8);
+    ct.touch(N, 2);
   } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
     h.mask = __ldg(buf + N);  // valid bits 0-7 (leaf bits 8-15 never indexed)
     ct.add(VF_CTR_SVDAG_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 4);
+    ct.touch(N, 1);
   } else if (has_kind<KINDS>(K_NTREE) && kind == K_NTREE) {
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(buf + N));
     h.mask = (typename Header<KINDS>::Mask)((uint64_t)v.x | ((uint64_t)v.y << 32));
     h.base = v.z;
     ct.add(VF_CTR_NTREE_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 16);
+    ct.touch(N, 4);
   }
 }
 
@@ -446,6 +458,7 @@ struct Lane {
           occ = child != 0u;
           ct.add(VF_CTR_RAW_CELLS);
           ct.add(VF_CTR_FORMAT_BYTES, 4);
+          ct.touch((size_t)N + lin, 1);
         } else if (budget > 0) {
           // DF: within L1 distance `budget` of a cell whose nearest non-empty cell is that far
           // away, so empty without a memory access ("how many voxels can be
@@ -458,6 +471,7 @@ struct Lane {
           budget = (int)v.y;
           ct.add(VF_CTR_RAW_CELLS);
           ct.add(VF_CTR_FORMAT_BYTES, 8);
+          ct.touch((size_t)N + 2 * lin, 2);
         }
       } else {
         const uint32_t lin = lx + (ly << sx) + (lz << sxy);
@@ -471,10 +485,12 @@ struct Lane {
             child = __ldg(buf + N + 1u + rank);
             ct.add(VF_CTR_SVDAG_PTRS);
             ct.add(VF_CTR_FORMAT_BYTES, 4);
+            ct.touch(N + 1u + rank, 1);
           } else {
             child = hd.base + (last ? 1u : 4u) * rank;
           }
           if (last) {  // leaf TermInt -> next level's root
+            ct.touch(child, 1);
             child = __ldg(buf + child);
             ct.add(VF_CTR_LEAF_WORDS);
             ct.add(VF_CTR_FORMAT_BYTES, 4);
@@ -663,6 +679,7 @@ __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const Tra
   stage_tiers(p, s_tw);
   const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   Ctr<COUNT> ct;
+  ct.touch_map = p.touch;
   if (gid < n) {
     Lane<KINDS, RESTART, COUNT> L;
     uint32_t stk[VF_MAX_TIERS];
@@ -701,6 +718,7 @@ __global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceP
   __shared__ __align__(16) uint32_t s_tw[8 * VF_MAX_TIERS];
   stage_tiers(p, s_tw);
   Ctr<COUNT> ct;
+  ct.touch_map = p.touch;
   Lane<KINDS, RESTART, COUNT> L;
   uint32_t stk[VF_MAX_TIERS];
   const unsigned lane = threadIdx.x & 31u;
@@ -752,6 +770,26 @@ __global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceP
       atomicExch(work, 0ull);
       atomicExch(work + 1, 0ull);
     }
+  }
+}
+
+// ---- touch bitmap reduction (counting runs): distinct words = set bits; distinct 32-B sectors =
+// non-zero bytes (byte j of bitmap word i covers words 32i + 8j .. +7, one sector of the
+// 256-B-aligned buffer)
+__global__ void touch_count_kernel(const uint32_t* __restrict__ touch, uint64_t nw, unsigned long long* counters) {
+  unsigned long long words = 0, sectors = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t w = touch[i];
+    words += __popc(w);
+    sectors += ((w & 0xFFu) != 0) + ((w & 0xFF00u) != 0) + ((w & 0xFF0000u) != 0) + ((w & 0xFF000000u) != 0);
+  }
+  for (int o = 16; o; o >>= 1) {
+    words += __shfl_down_sync(0xffffffffu, words, o);
+    sectors += __shfl_down_sync(0xffffffffu, sectors, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(counters + VF_CTR_UNIQUE_WORDS, words);
+    atomicAdd(counters + VF_CTR_UNIQUE_SECTORS, sectors);
   }
 }
 
@@ -864,7 +902,7 @@ int persistent_blocks(KernelFn fn, int device) {
 }  // namespace
 
 vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags, cudaStream_t s,
-                       unsigned long long* counters, vf_payload* payload) {
+                       unsigned long long* counters, vf_payload* payload, uint32_t* touch) {
   if (n == 0) return VF_OK;
   uint32_t kinds = 0;
   for (uint32_t t = 0; t < h->fmt.n_tiers; ++t) kinds |= 1u << h->fmt.tiers[t].kind;
@@ -882,6 +920,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     }();
     TraceParams tp = h->tp;
     tp.payload = reinterpret_cast<uint2*>(payload);
+    tp.touch = touch;
     if (refill_env) tp.refill = (uint32_t)refill_env;
     const uint32_t slot = h->work_slot.fetch_add(1) % kWorkSlots;
     unsigned long long* work = h->work + 2 * slot;
@@ -901,6 +940,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     }
     TraceParams tp = h->tp;
     tp.payload = reinterpret_cast<uint2*>(payload);
+    tp.touch = touch;
     fn<<<(unsigned)blocks, threads, 0, s>>>(tp, h->buf, reinterpret_cast<const float4*>(rays),
                                             reinterpret_cast<int4*>(hits), n, counters, nullptr);
   }
@@ -917,6 +957,19 @@ vf_status read_exact_calls(unsigned long long* out, bool reset) {
   if (reset) {
     const unsigned long long z = 0;
     VF_CUDA_TRY(cudaMemcpyToSymbol(g_exact_calls, &z, sizeof(z)));
+  }
+  return VF_OK;
+}
+
+vf_status launch_touch_count(const uint32_t* touch, uint64_t nw, unsigned long long* counters, cudaStream_t s) {
+  if (nw == 0) return VF_OK;
+  uint64_t blocks = (nw + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  touch_count_kernel<<<(unsigned)blocks, 256, 0, s>>>(touch, nw, counters);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("vf_trace_counters: touch count launch failed: %s", cudaGetErrorString(e));
+    return VF_ERR_CUDA;
   }
   return VF_OK;
 }

@@ -33,7 +33,7 @@ VF_MAX_LEVELS = 16
 VF_MAX_TIERS = 16
 COUNTER_NAMES = ("rays", "hits", "cell_tests", "steps", "descents", "pops", "redescents", "locates", "near_ties",
                  "raw_cells", "svo_nodes", "svdag_nodes", "svdag_ptrs", "ntree_nodes", "leaf_words", "format_bytes",
-                 "exact_calls", "warp_max_tests", "df_skips")
+                 "exact_calls", "warp_max_tests", "df_skips", "sector_reads", "unique_words", "unique_sectors")
 VF_NCOUNTERS = len(COUNTER_NAMES)
 
 
