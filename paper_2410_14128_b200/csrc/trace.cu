@@ -669,7 +669,10 @@ __device__ __forceinline__ void stage_tiers(const TraceParams& p, uint32_t* s_tw
 #ifndef VF_MINB
 #define VF_MINB 8  // __launch_bounds__ min blocks per SM (register cap), A/B-tuned
 #endif
-constexpr unsigned kTraceThreads = 128;
+#ifndef VF_TRACE_THREADS
+#define VF_TRACE_THREADS 128  // block size (A/B: 256 with VF_MINB 4 keeps the 64-register cap)
+#endif
+constexpr unsigned kTraceThreads = VF_TRACE_THREADS;
 template <uint32_t KINDS, bool RESTART, bool COUNT>
 __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
@@ -931,7 +934,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     static const unsigned threads = [] {
       const char* e = getenv("VF_BLOCK");
       const int v = e ? atoi(e) : 0;
-      return (v == 32 || v == 64 || v == 128) ? (unsigned)v : kTraceThreads;
+      return (v == 32 || v == 64 || (v > 0 && v <= (int)kTraceThreads && v % 32 == 0)) ? (unsigned)v : kTraceThreads;
     }();
     const uint64_t blocks = (n + threads - 1) / threads;
     if (blocks > 0x7fffffffull) {
