@@ -711,9 +711,12 @@ __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const Tra
 // warp ends, and the launch tail (SURVEY.md §8(d) "warp ballot early-out / persistent refill").
 // work[0] = next ray, work[1] = finished blocks; the last block resets both.
 constexpr int kPersistThreads = 128;
+#ifndef VF_PMINB
+#define VF_PMINB 8  // persistent kernel: min blocks per SM (register cap), A/B on incoherent rays
+#endif
 
 template <uint32_t KINDS, bool RESTART, bool COUNT>
-__global__ void __launch_bounds__(kPersistThreads) trace_persistent(const TraceParams p, const uint32_t* __restrict__ buf,
+__global__ void __launch_bounds__(kPersistThreads, VF_PMINB) trace_persistent(const TraceParams p, const uint32_t* __restrict__ buf,
                                                                    const float4* __restrict__ rays,
                                                                    int4* __restrict__ hits, uint64_t n,
                                                                    unsigned long long* __restrict__ counters,
