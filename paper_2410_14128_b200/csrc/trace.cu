@@ -130,7 +130,7 @@ __device__ __forceinline__ int cmp_events(const float (&o)[3], const float (&d)[
 
 // Exact argmin of the three next-plane events (ties step together). c = candidate mask (>= 2
 // bits). Returns the set of minimal axes | (one minimal axis << 4).
-__device__ __forceinline__ int argmin_exact(float o0, float o1, float o2, float d0, float d1, float d2, int P0, int P1,
+__device__ __noinline__ int argmin_exact(float o0, float o1, float o2, float d0, float d1, float d2, int P0, int P1,
                                          int P2, float t0, float t1, float t2, int c) {
   const float o[3] = {o0, o1, o2}, d[3] = {d0, d1, d2}, t[3] = {t0, t1, t2};
   const int P[3] = {P0, P1, P2};
@@ -154,6 +154,55 @@ __device__ __forceinline__ int argmin_exact(float o0, float o1, float o2, float 
     }
   }
   return set | (best << 4);
+}
+
+// Certified correction of a sub-cell locate when the fast path cannot decide (ray on / near a
+// plane at the event E; ~0.2 % of locates). Out of line and with scalar arguments only, so the
+// hot loop stays compact and the lane state stays in registers. Finds k in [lo, hi] with
+//   d_b > 0: T_b(k) <= E < T_b(k+1);   d_b < 0: T_b(k+1) <= E < T_b(k)
+// by certified comparisons of E = {axis ea, plane eP (or tmin: ea = TMIN_AXIS), fp32 value et}
+// against plane events of axis b (b != ea: the event axis is never located).
+__device__ __noinline__ int locate_slow(float ob, float db, float invb, int lo, int hi, int ea, int eP, float et,
+                                        float oe, float de) {
+  // sign(E - T_b(Q))
+  auto cmp = [&](int Q) {
+    const float tq = tplane(Q, ob, invb);
+    const int c = cert(et, tq);
+    if (c != 2) return c;
+    if (ea == TMIN_AXIS) return -cmp_ps_exact(Q, ob, db, et);
+    return cmp_pp_exact(eP, oe, de, Q, ob, db);
+  };
+  const float x = fmaf(et, db, ob);
+  const float fl = floorf(x);
+  float kf = db > 0.f ? fl : ceilf(x) - 1.0f;
+  kf = fminf(fmaxf(kf, (float)lo), (float)hi);
+  int k = (int)kf;
+  if (db > 0.f) {
+    for (;;) {
+      if (k > lo && cmp(k) < 0) {
+        --k;
+        continue;
+      }
+      if (k < hi && cmp(k + 1) >= 0) {
+        ++k;
+        continue;
+      }
+      break;
+    }
+  } else {
+    for (;;) {
+      if (k < hi && cmp(k + 1) < 0) {
+        ++k;
+        continue;
+      }
+      if (k > lo && cmp(k) >= 0) {
+        --k;
+        continue;
+      }
+      break;
+    }
+  }
+  return k;
 }
 
 __device__ __forceinline__ uint32_t field4(uint64_t pack, uint32_t i) { return (uint32_t)(pack >> (4 * i)) & 15u; }
@@ -315,36 +364,11 @@ struct Lane {
     const float f = x - fl;  // exact
     const float B = (fabsf(et * db) + fabsf(x)) * 0x1p-21f;
     int k = (int)fl;
-    if (f > B && 1.0f - f > B && k >= lo && k <= hi) return k;
-    float kf = db > 0.f ? fl : ceilf(x) - 1.0f;
-    kf = fminf(fmaxf(kf, (float)lo), (float)hi);
-    k = (int)kf;
-    if (db > 0.f) {
-      for (;;) {
-        if (k > lo && cmp_eq(b, k) < 0) {
-          --k;
-          continue;
-        }
-        if (k < hi && cmp_eq(b, k + 1) >= 0) {
-          ++k;
-          continue;
-        }
-        break;
-      }
-    } else {
-      for (;;) {
-        if (k < hi && cmp_eq(b, k + 1) < 0) {
-          ++k;
-          continue;
-        }
-        if (k > lo && cmp_eq(b, k) >= 0) {
-          --k;
-          continue;
-        }
-        break;
-      }
-    }
-    return k;
+    // (no range test: certified, floor(x^) is the exact tau_b(E+), and the ray is inside the cell
+    //  [lo, hi] on axis b at E+ by the traversal invariant; the range only bounds the slow path)
+    if (f > B && 1.0f - f > B) return k;
+    return locate_slow(ob, db, sel3(inv, b), lo, hi, eaxis, eaxis == TMIN_AXIS ? 0 : eplane(),
+                       et, eaxis == TMIN_AXIS ? 0.f : sel3(o, eaxis), eaxis == TMIN_AXIS ? 1.f : sel3(d, eaxis));
   }
 
   // s_tw: the tier table staged in shared memory, two uint4 per tier (stage_tiers): one LDS.128
