@@ -302,8 +302,14 @@ enum { IT_CONTINUE = 0, IT_HIT = 1, IT_MISS = 2 };
 // on axis eaxis, or tmin (eaxis = TMIN_AXIS). Its plane is not stored: the cell entered through
 // it is V[eaxis], so the plane is V[eaxis] + (d < 0) — the event axis never goes stale, and
 // descents and pops do not move V. The exact fallbacks rebuild it from there.
-template <uint32_t KINDS, bool RESTART, bool COUNT>
+//
+// SPEC != 0 compiles the format in: SPEC = A << 8 | M is R(A^3) G(M) (a cubic Raw top level over
+// an SVDAG of depth M, the paper's recommended family), whose tier geometry is arithmetic
+// in the tier index t (lc = M - t, 2x2x2 cells below tier 0) — the paper's generated
+// per-format code (§4) as a template instance; no tier table, fewer live registers.
+template <uint32_t KINDS, bool RESTART, bool COUNT, uint32_t SPEC = 0>
 struct Lane {
+  static constexpr uint32_t SA = SPEC >> 8, SM = SPEC & 255u;
   float o[3], d[3], inv[3];  // inv = RN(1/d); +inf on axes with d = 0 (their next plane is never)
   float tmax;
   int V[3];       // finest voxel of the current cell (bits below lc(t) valid unless stale)
@@ -311,8 +317,27 @@ struct Lane {
   float et;       // its fp32 time fl(fl(P - o) * inv) (or tmin)
   int t;          // current tier
   uint32_t N;     // current node (word address)
-  uint32_t tw;    // tier word of tier t
-  uint32_t lc, msk, sx, sxy;  // decoded from tw
+  uint32_t tw;    // tier word of tier t (generic formats)
+  uint32_t lc_, msk_, sx_, sxy_;  // decoded from tw (generic formats)
+
+  // tier geometry and flags of tier t (compile-time arithmetic for SPEC formats)
+  __device__ __forceinline__ uint32_t lc() const { return SPEC ? SM - (uint32_t)t : lc_; }
+  __device__ __forceinline__ uint32_t msk() const { return SPEC ? (t == 0 ? (1u << SA) - 1u : 1u) : msk_; }
+  __device__ __forceinline__ uint32_t sx() const { return SPEC ? (t == 0 ? SA : 1u) : sx_; }
+  __device__ __forceinline__ uint32_t sxy() const { return SPEC ? (t == 0 ? 2u * SA : 2u) : sxy_; }
+  __device__ __forceinline__ uint32_t kind() const { return SPEC ? (t == 0 ? (uint32_t)K_RAW : (uint32_t)K_SVDAG) : (tw & 3u); }
+  __device__ __forceinline__ bool finest() const { return SPEC ? t == (int)SM : (tw & TW_FINEST) != 0; }
+  __device__ __forceinline__ bool last() const { return SPEC ? (t == 0 || t == (int)SM) : (tw & TW_LAST) != 0; }
+  __device__ __forceinline__ bool is_df() const { return SPEC ? false : (tw & TW_DF) != 0; }
+  __device__ __forceinline__ bool is_top() const { return SPEC ? t <= 1 : (tw & TW_TOP) != 0; }
+  __device__ __forceinline__ uint32_t lcp() const { return SPEC ? (t == 0 ? 15u : SM + 1u - (uint32_t)t) : twf(tw, TW_LCP, 4); }
+  // deepest tier whose node holds two cells first differing at bit h; the top tier of its level
+  __device__ __forceinline__ int tau(const TraceParams& p, uint32_t h) const {
+    return SPEC ? (h >= SM ? 0 : (int)(SM - h)) : (int)field4(p.tau_pack, h);
+  }
+  __device__ __forceinline__ int level_top(const TraceParams& p, int tu) const {
+    return SPEC ? (tu == 0 ? 0 : 1) : (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tu);
+  }
   Header<KINDS> hd;
   int stale;          // axes whose bits below stale_lc are not exact at E
   uint32_t stale_lc;  // bits of V below this are stale on the axes in `stale`
@@ -375,12 +400,14 @@ struct Lane {
   // and one LDS.32 per tier change instead of extracting the fields from the tier word.
   __device__ __forceinline__ void set_tier(const uint32_t* s_tw, int nt) {
     t = nt;
-    const uint4 a = reinterpret_cast<const uint4*>(s_tw)[2 * nt];
-    tw = a.x;
-    lc = a.y;
-    msk = a.z;
-    sx = a.w;
-    sxy = s_tw[8 * nt + 4];
+    if (!SPEC) {
+      const uint4 a = reinterpret_cast<const uint4*>(s_tw)[2 * nt];
+      tw = a.x;
+      lc_ = a.y;
+      msk_ = a.z;
+      sx_ = a.w;
+      sxy_ = s_tw[8 * nt + 4];
+    }
     budget = 0;
   }
 
@@ -452,32 +479,32 @@ struct Lane {
     N = p.root;
     hd.mask = 0;
     hd.base = 0;
-    load_header<KINDS>(buf, tw & 3u, N, hd, ct);
+    load_header<KINDS>(buf, kind(), N, hd, ct);
     stale = 0;
     stale_lc = 0;
     return true;
   }
 
-  // Invariant: V >> lc is the current (untested) cell of node N at tier t, entered at E (the
+  // Invariant: V >> lc() is the current (untested) cell of node N at tier t, entered at E (the
   // tier-change block below re-derives stale sub-cell bits right after a descent).
   // A pop always follows a step, so it lands on a new cell.
   __device__ __forceinline__ int iterate(const TraceParams& p, const uint32_t* __restrict__ buf,
                                          const uint32_t* s_tw, uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
     int nt = t;       // tier after this iteration
     uint32_t nN = N;  // node after this iteration
-    const uint32_t kind = tw & 3u;
-    const bool finest = tw & TW_FINEST;
+    const uint32_t kind = this->kind();
+    const bool finest = this->finest();
     {
       // -- test the current cell of the current node (ordered_hit_children, one child)
-      const uint32_t lx = ((uint32_t)V[0] >> lc) & msk, ly = ((uint32_t)V[1] >> lc) & msk,
-                     lz = ((uint32_t)V[2] >> lc) & msk;
+      const uint32_t lx = ((uint32_t)V[0] >> lc()) & msk(), ly = ((uint32_t)V[1] >> lc()) & msk(),
+                     lz = ((uint32_t)V[2] >> lc()) & msk();
       bool occ = false;
       uint32_t child = 0;
       ct.add(VF_CTR_CELL_TESTS);
       if (has_kind<KINDS>(K_RAW) && kind == K_RAW) {
         // 64-bit index: a single-level R(11^3) grid has 2^33 cells (reading A15)
-        const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
-        if (!(tw & TW_DF)) {
+        const size_t lin = (size_t)lx + ((size_t)ly << sx()) + ((size_t)lz << sxy());
+        if (!is_df()) {
           child = __ldg(buf + (size_t)N + lin);
           occ = child != 0u;
           ct.add(VF_CTR_RAW_CELLS);
@@ -498,11 +525,11 @@ struct Lane {
           ct.touch((size_t)N + 2 * lin, 2);
         }
       } else {
-        const uint32_t lin = lx + (ly << sx) + (lz << sxy);
+        const uint32_t lin = lx + (ly << sx()) + (lz << sxy());
         occ = (hd.mask >> lin) & 1u;
         if (occ && !finest) {
           const uint32_t rank = hd.rank(lin);
-          const bool last = tw & TW_LAST;
+          const bool last = this->last();
           if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
             child = hd.base + 2u * rank;
           } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
@@ -524,7 +551,7 @@ struct Lane {
       if (occ) {
         if (finest) return IT_HIT;  // unit intersection
         // descend at event E (the child's entry cell is derived at the top of the next iteration)
-        if (!RESTART || (tw & TW_TOP)) stk[t] = N;
+        if (!RESTART || is_top()) stk[t] = N;
         nt = t + 1;
         nN = child;
         ct.add(VF_CTR_DESCENTS);
@@ -538,19 +565,19 @@ struct Lane {
     if (nt != t) {
       set_tier(s_tw, nt);
       N = nN;
-      load_header<KINDS>(buf, tw & 3u, N, hd, ct);
-      // after a descent, the new tier's cell needs V's bits >= lc; if some of those are stale (the
+      load_header<KINDS>(buf, this->kind(), N, hd, ct);
+      // after a descent, the new tier's cell needs V's bits >= lc(); if some of those are stale (the
       // ray moved inside a cell of size 2^stale_lc since they were exact), derive the exact finest
       // voxel of the stale axes within the parent cell (edge 2^lc(t-1); bits above it exact).
-      // (never true after a pop: a pop lands on a tier with lc >= stale_lc)
-      if (stale && lc < stale_lc) {
-        const uint32_t lcp = twf(tw, TW_LCP, 4);
+      // (never true after a pop: a pop lands on a tier with lc() >= stale_lc)
+      if (stale && lc() < stale_lc) {
+        const uint32_t pl = lcp();
         const int st = stale & moving;
 #pragma unroll
         for (int b = 0; b < 3; ++b)
           if ((st >> b) & 1) {
-            const int lo = (V[b] >> lcp) << lcp;
-            V[b] = locate(b, lo, lo + (1 << lcp) - 1);
+            const int lo = (V[b] >> pl) << pl;
+            V[b] = locate(b, lo, lo + (1 << pl) - 1);
             ct.add(VF_CTR_LOCATES);
           }
         stale = 0;
@@ -570,7 +597,7 @@ struct Lane {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       // next plane on axis a at this tier's cell size (inv = +inf makes a d = 0 axis never step)
-      Pn[a] = ((V[a] >> lc) + 1 - ((dneg >> a) & 1)) << lc;
+      Pn[a] = ((V[a] >> lc()) + 1 - ((dneg >> a) & 1)) << lc();
       tn[a] = tplane(Pn[a], o[a], inv[a]);
     }
     const float m = fminf(fminf(tn[0], tn[1]), tn[2]);
@@ -612,24 +639,24 @@ struct Lane {
       return;
     }
     // (axes with d = 0 may be marked too: they never move, and the locate block skips them)
-    if (lc) {
+    if (lc()) {
       stale |= ~S & 7;
-      stale_lc = max(stale_lc, lc);
+      stale_lc = max(stale_lc, lc());
     }
     stale &= ~S;
     budget -= __popc(S);  // L1 distance moved (DF tiers only use it)
     // h = highest bit in which the old and new cells differ; the step leaves this tier's node iff
     // h >= lc(t-1) (the node's edge), and then tau(h) is the deepest tier whose node holds both
     const uint32_t h = 31u - __clz((uint32_t)x);
-    if (h >= twf(tw, TW_LCP, 4)) {
-      const int tau = (int)field4(p.tau_pack, h);
+    if (h >= lcp()) {
+      const int tu = tau(p, h);
       ct.add(VF_CTR_POPS);
       // left the current node: pop (stack) or restart from the level root
       // (restart: from the top of tau's level — the following iterations re-descend through the
       //  nodes that contain the current cell as ordinary, always-occupied descents)
-      nt = RESTART ? (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tau) : tau;
+      nt = RESTART ? level_top(p, tu) : tu;
       nN = stk[nt];
-      if (RESTART) ct.add(VF_CTR_REDESCENTS, tau - nt);
+      if (RESTART) ct.add(VF_CTR_REDESCENTS, tu - nt);
     }
   }
 
@@ -640,15 +667,15 @@ struct Lane {
   // axis whose plane event entered the hit cell (lowest axis on exact ties; 0 when the segment
   // starts inside the hit cell at tmin). Evaluated once per hit, at the finest tier.
   __device__ __forceinline__ uint2 payload_record(const uint32_t* __restrict__ buf) const {
-    const uint32_t lx = ((uint32_t)V[0] >> lc) & msk, ly = ((uint32_t)V[1] >> lc) & msk,
-                   lz = ((uint32_t)V[2] >> lc) & msk;
-    const uint32_t kind = tw & 3u;
+    const uint32_t lx = ((uint32_t)V[0] >> lc()) & msk(), ly = ((uint32_t)V[1] >> lc()) & msk(),
+                   lz = ((uint32_t)V[2] >> lc()) & msk();
+    const uint32_t kind = this->kind();
     uint32_t rgba = 0;
     if (kind == K_RAW) {
-      const size_t lin = (size_t)lx + ((size_t)ly << sx) + ((size_t)lz << sxy);
-      rgba = __ldg(buf + (size_t)N + lin * ((tw & TW_DF) ? 2u : 1u));
+      const size_t lin = (size_t)lx + ((size_t)ly << sx()) + ((size_t)lz << sxy());
+      rgba = __ldg(buf + (size_t)N + lin * (is_df() ? 2u : 1u));
     } else {
-      const uint32_t lin = lx + (ly << sx) + (lz << sxy);
+      const uint32_t lin = lx + (ly << sx()) + (lz << sxy());
       const uint32_t rank = hd.rank(lin);
       if (kind == K_SVO)
         rgba = __ldg(buf + hd.base + 2u * rank);
@@ -697,7 +724,7 @@ __device__ __forceinline__ void stage_tiers(const TraceParams& p, uint32_t* s_tw
 #define VF_TRACE_THREADS 128  // block size (A/B: 256 with VF_MINB 4 keeps the 64-register cap)
 #endif
 constexpr unsigned kTraceThreads = VF_TRACE_THREADS;
-template <uint32_t KINDS, bool RESTART, bool COUNT>
+template <uint32_t KINDS, bool RESTART, bool COUNT, uint32_t SPEC = 0>
 __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
                                                     uint64_t n, unsigned long long* __restrict__ counters,
@@ -708,7 +735,7 @@ __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const Tra
   Ctr<COUNT> ct;
   ct.touch_map = p.touch;
   if (gid < n) {
-    Lane<KINDS, RESTART, COUNT> L;
+    Lane<KINDS, RESTART, COUNT, SPEC> L;
     uint32_t stk[VF_MAX_TIERS];
     int4 out = miss_record();
     if (L.start(p, buf, s_tw, __ldg(rays + 2 * gid), __ldg(rays + 2 * gid + 1), ct)) {
@@ -909,6 +936,30 @@ KernelFn select_kernel(uint32_t kinds, bool restart, bool count, bool persistent
 #endif
 }
 
+// Compiled-in formats (Lane SPEC): R(A^3) G(M) with a cubic root, no DF — the cfg4 / cfg5 / t512
+// headline formats and their neighbours in the sweeps. Other formats run the generic kernel.
+template <uint32_t SPEC>
+KernelFn spec_kernel(bool restart) {
+  return restart ? trace_kernel<5, true, false, SPEC> : trace_kernel<5, false, false, SPEC>;
+}
+
+KernelFn select_spec(const Format& f, bool restart) {
+#ifdef VF_ONLY_KINDS
+  if (VF_ONLY_KINDS != 5) return nullptr;
+#endif
+  if (f.n_levels != 2 || f.levels[0].kind != VF_RAW || f.levels[1].kind != VF_SVDAG) return nullptr;
+  const uint8_t* e = f.levels[0].log2_extent;
+  if (e[0] != e[1] || e[1] != e[2]) return nullptr;
+  switch (((uint32_t)e[0] << 8) | f.levels[1].depth) {
+#define VF_SPEC(a, m) \
+  case ((a) << 8) | (m): return spec_kernel<((a) << 8) | (m)>(restart);
+    VF_SPEC(4, 7) VF_SPEC(4, 8) VF_SPEC(3, 8) VF_SPEC(3, 7) VF_SPEC(4, 5) VF_SPEC(2, 7) VF_SPEC(6, 5)
+    VF_SPEC(2, 3) VF_SPEC(1, 4)  // small instances for the parity tests
+#undef VF_SPEC
+    default: return nullptr;
+  }
+}
+
 // resident blocks per SM for a persistent kernel (cached per function and device)
 int persistent_blocks(KernelFn fn, int device) {
   struct Entry {
@@ -938,6 +989,9 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
   for (uint32_t t = 0; t < h->fmt.n_tiers; ++t) kinds |= 1u << h->fmt.tiers[t].kind;
   const bool persistent = (flags & (VF_TRACE_PERSISTENT_WARPS | VF_TRACE_INCOHERENT)) != 0;
   KernelFn fn = select_kernel(kinds, (flags & VF_TRACE_RESTART_SV) != 0, counters != nullptr, persistent);
+  static const bool no_spec = getenv("VF_NO_SPEC") != nullptr;  // A/B and tests: generic kernel only
+  if (!persistent && !counters && !no_spec)
+    if (KernelFn sf = select_spec(h->fmt, (flags & VF_TRACE_RESTART_SV) != 0)) fn = sf;
   if (!fn) {
     set_error("vf_trace: no kernel instantiated for kind set 0x%x", kinds);
     return VF_ERR_UNSUPPORTED;

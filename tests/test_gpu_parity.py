@@ -370,3 +370,50 @@ def test_payload_rgba_and_entry_face(fmt):
         assert (pay[~hit] == 0).all()
         nrm = np.ascontiguousarray(pay[:, 1]).view(np.uint8).reshape(-1, 4)[:, :3].view(np.int8)
         np.testing.assert_array_equal(nrm, ref["normal"])
+
+
+# ---------------------------------------------------------------- compiled-in formats (Lane SPEC)
+@pytest.mark.parametrize("fmt,dims", [("R(2^3) G(3)", 32), ("R(1^3) G(4)", 32)])
+@pytest.mark.parametrize("p", [0.02, 0.3])
+def test_compiled_in_format_vs_oracle(fmt, dims, p):
+    """R(A^3) G(M) formats run a kernel with the format compiled in (trace.cu select_spec: tier
+    geometry as arithmetic in the tier index). Same oracle parity as the generic kernel, stack and
+    restart, payload included; the generic kernel (VF_NO_SPEC, subprocess) returns the same bits."""
+    import os
+    import subprocess
+    import sys
+    import torch
+    vf = _vf()
+    d = inputs.random_occupancy((dims,) * 3, p, 4321)
+    dense = inputs.dense_host(d)
+    h = vf.build(torch.from_numpy(dense.view(np.int32)).cuda(), fmt)
+    rays = np.concatenate([R.adversarial_rays(6000, (dims,) * 3, 3), R.random_rays(4000, (dims,) * 3, 4)])
+    ref = oracle.Grid.from_generator(d).trace(rays)
+    rt = torch.from_numpy(rays).cuda()
+    outs = []
+    for restart in (False, True):
+        hits, pay = h.trace_payload(rt, restart=restart)
+        hits, pay = hits.cpu().numpy(), pay.cpu().numpy()
+        assert_parity(hits[:, :3], hits[:, 3].view(np.float32), ref, f"{fmt} restart={restart}")
+        hit = ref["xyz"][:, 0] >= 0
+        x, y, z = ref["xyz"][hit].T
+        np.testing.assert_array_equal(np.ascontiguousarray(pay[hit, 0]).view(np.uint32), dense[z, y, x])
+        out = h.trace(rt, restart=restart).cpu().numpy()
+        np.testing.assert_array_equal(out, hits)
+        outs.append(out)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np, torch; sys.path.insert(0, sys.argv[1]); import inputs; "
+            "from paper_2410_14128_b200 import vf; d = inputs.random_occupancy((%d,) * 3, %r, 4321); "
+            "h = vf.build(torch.from_numpy(inputs.dense_host(d).view(np.int32)).cuda(), %r); "
+            "r = torch.from_numpy(np.load(sys.argv[2])).cuda(); "
+            "np.save(sys.argv[3], np.stack([h.trace(r, restart=s).cpu().numpy() for s in (False, True)]))"
+            % (dims, p, fmt))
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        np.save(os.path.join(td, "r.npy"), rays)
+        rr = subprocess.run([sys.executable, "-c", code, root, os.path.join(td, "r.npy"), os.path.join(td, "o.npy")],
+                            env=dict(os.environ, VF_NO_SPEC="1"), capture_output=True, text=True, timeout=300)
+        assert rr.returncode == 0, rr.stderr[-2000:]
+        gen = np.load(os.path.join(td, "o.npy"))
+    np.testing.assert_array_equal(gen[0], outs[0])
+    np.testing.assert_array_equal(gen[1], outs[1])
