@@ -233,7 +233,11 @@ def run_ours(args):
 
     # N > 1: the frame's trace and its hit gather are pipelined over K row chunks of the rank's
     # (padded) hit buffer — chunk k's NCCL gather overlaps the trace of chunk k+1.
-    pipe = shard.ChunkedGather(counts, args.gather_chunks, dev) if world > 1 else None
+    # K = --gather-chunks, or auto: one chunk per 512k local rays (at most 4) — a trace launch
+    # lasts at least as long as its slowest ray, so chunks much smaller than that cost more in
+    # launch tails than the overlap with the gather returns
+    k_chunks = args.gather_chunks if args.gather_chunks > 0 else max(1, min(4, max(counts) // (1 << 19)))
+    pipe = shard.ChunkedGather(counts, k_chunks, dev) if world > 1 else None
     if pipe is not None:
         hits = pipe.hits
 
@@ -542,7 +546,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-format sweep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--gather-chunks", type=int, default=4, help="N>1: trace/gather pipeline depth")
+    ap.add_argument("--gather-chunks", type=int, default=0, help="N>1: trace/gather pipeline depth (0: auto)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
