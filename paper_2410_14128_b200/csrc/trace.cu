@@ -291,6 +291,105 @@ __device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, ui
   }
 }
 
+// ---- compiled-in formats (the paper's per-format generated code, §4, as template instances) --
+// A format descriptor D gives the tier geometry and flags as functions of the tier index t:
+//   NoSpec        — generic: read from the tier table (any format)
+//   RawSvdag<A,M> — R(A^3) G(M): lc = M - t, 2x2x2 cells below tier 0 (pure arithmetic)
+//   Packed<...>   — any cubic format of <= 8 tiers without DF: per-tier fields packed into
+//                   compile-time immediates (4 bits per tier), extracted with a shift and a mask
+struct NoSpec {
+  static constexpr bool kStatic = false;
+};
+
+template <uint32_t A, uint32_t M>
+struct RawSvdag {
+  static constexpr bool kStatic = true;
+  __device__ static __forceinline__ uint32_t lc(int t) { return M - (uint32_t)t; }
+  __device__ static __forceinline__ uint32_t msk(int t) { return t == 0 ? (1u << A) - 1u : 1u; }
+  __device__ static __forceinline__ uint32_t sx(int t) { return t == 0 ? A : 1u; }
+  __device__ static __forceinline__ uint32_t sxy(int t) { return t == 0 ? 2u * A : 2u; }
+  __device__ static __forceinline__ uint32_t kind(int t) { return t == 0 ? (uint32_t)K_RAW : (uint32_t)K_SVDAG; }
+  __device__ static __forceinline__ bool finest(int t) { return t == (int)M; }
+  __device__ static __forceinline__ bool last(int t) { return t == 0 || t == (int)M; }
+  __device__ static __forceinline__ bool top(int t) { return t <= 1; }
+  __device__ static __forceinline__ uint32_t lcp(int t) { return t == 0 ? 15u : M + 1u - (uint32_t)t; }
+  __device__ static __forceinline__ int tau(uint32_t h) { return h >= M ? 0 : (int)(M - h); }
+  __device__ static __forceinline__ int level_top(int tu) { return tu == 0 ? 0 : 1; }
+};
+
+struct LevelSpec {
+  uint32_t kind, lf, depth;  // VF_RAW / VF_SVO / VF_SVDAG / VF_NTREE, log2 fan-out per axis, tiers
+};
+struct Packs {
+  uint32_t nt, lc, lf, kind, last, top, lcp, ltop, tau_lo, tau_hi;
+};
+// Tier tables of a cubic level list (the same expansion as format.cu, at compile time).
+template <size_t NL>
+constexpr Packs make_packs(const LevelSpec (&lv)[NL]) {
+  uint32_t kind[VF_MAX_TIERS] = {}, lf[VF_MAX_TIERS] = {}, top[VF_MAX_TIERS] = {}, last[VF_MAX_TIERS] = {},
+           ltop[VF_MAX_TIERS] = {}, lc[VF_MAX_TIERS] = {};
+  uint32_t nt = 0, total = 0;
+  for (size_t l = 0; l < NL; ++l) {
+    const uint32_t k = lv[l].kind == VF_RAW ? K_RAW : lv[l].kind == VF_SVO ? K_SVO : lv[l].kind == VF_SVDAG ? K_SVDAG : K_NTREE;
+    const uint32_t f = (lv[l].kind == VF_SVO || lv[l].kind == VF_SVDAG) ? 1u : lv[l].lf;
+    const uint32_t d = lv[l].kind == VF_RAW ? 1u : lv[l].depth;
+    for (uint32_t i = 0; i < d; ++i) {
+      kind[nt] = k;
+      lf[nt] = f;
+      top[nt] = i == 0;
+      last[nt] = i + 1 == d;
+      ltop[nt] = nt - i;
+      total += f;
+      ++nt;
+    }
+  }
+  uint32_t rem = total;
+  for (uint32_t t = 0; t < nt; ++t) {
+    rem -= lf[t];
+    lc[t] = rem;
+  }
+  Packs p{};
+  p.nt = nt;
+  for (uint32_t t = 0; t < nt; ++t) {
+    p.lc |= lc[t] << (4 * t);
+    p.lf |= lf[t] << (4 * t);
+    p.kind |= kind[t] << (4 * t);
+    p.last |= last[t] << t;
+    p.top |= top[t] << t;
+    p.lcp |= (t ? lc[t - 1] : 15u) << (4 * t);
+    p.ltop |= ltop[t] << (4 * t);
+  }
+  for (uint32_t h = 0; h < 16; ++h) {
+    uint32_t tu = 0;
+    for (uint32_t t = 1; t < nt; ++t)
+      if (lc[t - 1] > h) tu = t;
+    if (h < 8)
+      p.tau_lo |= tu << (4 * h);
+    else
+      p.tau_hi |= tu << (4 * (h - 8));
+  }
+  return p;
+}
+
+template <uint32_t NT, uint32_t LC, uint32_t LF, uint32_t KIND, uint32_t LAST, uint32_t TOP, uint32_t LCP,
+          uint32_t LTOP, uint32_t TAU_LO, uint32_t TAU_HI>
+struct Packed {
+  static constexpr bool kStatic = true;
+  __device__ static __forceinline__ uint32_t f4(uint32_t pack, int t) { return (pack >> (4 * t)) & 15u; }
+  __device__ static __forceinline__ uint32_t lc(int t) { return f4(LC, t); }
+  __device__ static __forceinline__ uint32_t msk(int t) { return (1u << f4(LF, t)) - 1u; }
+  __device__ static __forceinline__ uint32_t sx(int t) { return f4(LF, t); }
+  __device__ static __forceinline__ uint32_t sxy(int t) { return 2u * f4(LF, t); }
+  __device__ static __forceinline__ uint32_t kind(int t) { return f4(KIND, t); }
+  __device__ static __forceinline__ bool finest(int t) { return t == (int)NT - 1; }
+  __device__ static __forceinline__ bool last(int t) { return (LAST >> t) & 1u; }
+  __device__ static __forceinline__ bool top(int t) { return (TOP >> t) & 1u; }
+  __device__ static __forceinline__ uint32_t lcp(int t) { return f4(LCP, t); }
+  __device__ static __forceinline__ int tau(uint32_t h) { return (int)(h < 8 ? f4(TAU_LO, h) : f4(TAU_HI, h - 8)); }
+  __device__ static __forceinline__ int level_top(int tu) { return (int)f4(LTOP, tu); }
+};
+#define VF_PACKED(P) Packed<P.nt, P.lc, P.lf, P.kind, P.last, P.top, P.lcp, P.ltop, P.tau_lo, P.tau_hi>
+
 enum { IT_CONTINUE = 0, IT_HIT = 1, IT_MISS = 2 };
 
 // The per-ray traversal state machine: start() is the root function, iterate() is one cell test
@@ -303,13 +402,11 @@ enum { IT_CONTINUE = 0, IT_HIT = 1, IT_MISS = 2 };
 // it is V[eaxis], so the plane is V[eaxis] + (d < 0) — the event axis never goes stale, and
 // descents and pops do not move V. The exact fallbacks rebuild it from there.
 //
-// SPEC != 0 compiles the format in: SPEC = A << 8 | M is R(A^3) G(M) (a cubic Raw top level over
-// an SVDAG of depth M, the paper's recommended family), whose tier geometry is arithmetic
-// in the tier index t (lc = M - t, 2x2x2 cells below tier 0) — the paper's generated
-// per-format code (§4) as a template instance; no tier table, fewer live registers.
-template <uint32_t KINDS, bool RESTART, bool COUNT, uint32_t SPEC = 0>
+// D (a format descriptor above) compiles the format in: with D::kStatic the tier geometry and
+// flags are functions of the tier index (no tier table, fewer live registers).
+template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec>
 struct Lane {
-  static constexpr uint32_t SA = SPEC >> 8, SM = SPEC & 255u;
+  static constexpr bool SPEC = D::kStatic;
   float o[3], d[3], inv[3];  // inv = RN(1/d); +inf on axes with d = 0 (their next plane is never)
   float tmax;
   int V[3];       // finest voxel of the current cell (bits below lc(t) valid unless stale)
@@ -320,24 +417,46 @@ struct Lane {
   uint32_t tw;    // tier word of tier t (generic formats)
   uint32_t lc_, msk_, sx_, sxy_;  // decoded from tw (generic formats)
 
-  // tier geometry and flags of tier t (compile-time arithmetic for SPEC formats)
-  __device__ __forceinline__ uint32_t lc() const { return SPEC ? SM - (uint32_t)t : lc_; }
-  __device__ __forceinline__ uint32_t msk() const { return SPEC ? (t == 0 ? (1u << SA) - 1u : 1u) : msk_; }
-  __device__ __forceinline__ uint32_t sx() const { return SPEC ? (t == 0 ? SA : 1u) : sx_; }
-  __device__ __forceinline__ uint32_t sxy() const { return SPEC ? (t == 0 ? 2u * SA : 2u) : sxy_; }
-  __device__ __forceinline__ uint32_t kind() const { return SPEC ? (t == 0 ? (uint32_t)K_RAW : (uint32_t)K_SVDAG) : (tw & 3u); }
-  __device__ __forceinline__ bool finest() const { return SPEC ? t == (int)SM : (tw & TW_FINEST) != 0; }
-  __device__ __forceinline__ bool last() const { return SPEC ? (t == 0 || t == (int)SM) : (tw & TW_LAST) != 0; }
-  __device__ __forceinline__ bool is_df() const { return SPEC ? false : (tw & TW_DF) != 0; }
-  __device__ __forceinline__ bool is_top() const { return SPEC ? t <= 1 : (tw & TW_TOP) != 0; }
-  __device__ __forceinline__ uint32_t lcp() const { return SPEC ? (t == 0 ? 15u : SM + 1u - (uint32_t)t) : twf(tw, TW_LCP, 4); }
+  // tier geometry and flags of tier t
+  __device__ __forceinline__ uint32_t lc() const {
+    if constexpr (SPEC) return D::lc(t); else return lc_;
+  }
+  __device__ __forceinline__ uint32_t msk() const {
+    if constexpr (SPEC) return D::msk(t); else return msk_;
+  }
+  __device__ __forceinline__ uint32_t sx() const {
+    if constexpr (SPEC) return D::sx(t); else return sx_;
+  }
+  __device__ __forceinline__ uint32_t sxy() const {
+    if constexpr (SPEC) return D::sxy(t); else return sxy_;
+  }
+  __device__ __forceinline__ uint32_t kind() const {
+    if constexpr (SPEC) return D::kind(t); else return tw & 3u;
+  }
+  __device__ __forceinline__ bool finest() const {
+    if constexpr (SPEC) return D::finest(t); else return (tw & TW_FINEST) != 0;
+  }
+  __device__ __forceinline__ bool last() const {
+    if constexpr (SPEC) return D::last(t); else return (tw & TW_LAST) != 0;
+  }
+  __device__ __forceinline__ bool is_df() const {
+    if constexpr (SPEC) return false; else return (tw & TW_DF) != 0;
+  }
+  __device__ __forceinline__ bool is_top() const {
+    if constexpr (SPEC) return D::top(t); else return (tw & TW_TOP) != 0;
+  }
+  __device__ __forceinline__ uint32_t lcp() const {
+    if constexpr (SPEC) return D::lcp(t); else return twf(tw, TW_LCP, 4);
+  }
   // deepest tier whose node holds two cells first differing at bit h; the top tier of its level
   __device__ __forceinline__ int tau(const TraceParams& p, uint32_t h) const {
-    return SPEC ? (h >= SM ? 0 : (int)(SM - h)) : (int)field4(p.tau_pack, h);
+    if constexpr (SPEC) return D::tau(h); else return (int)field4(p.tau_pack, h);
   }
   __device__ __forceinline__ int level_top(const TraceParams& p, int tu) const {
-    return SPEC ? (tu == 0 ? 0 : 1) : (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tu);
+    if constexpr (SPEC) return D::level_top(tu);
+    else return (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tu);
   }
+
   Header<KINDS> hd;
   int stale;          // axes whose bits below stale_lc are not exact at E
   uint32_t stale_lc;  // bits of V below this are stale on the axes in `stale`
@@ -400,7 +519,7 @@ struct Lane {
   // and one LDS.32 per tier change instead of extracting the fields from the tier word.
   __device__ __forceinline__ void set_tier(const uint32_t* s_tw, int nt) {
     t = nt;
-    if (!SPEC) {
+    if constexpr (!SPEC) {
       const uint4 a = reinterpret_cast<const uint4*>(s_tw)[2 * nt];
       tw = a.x;
       lc_ = a.y;
@@ -724,7 +843,7 @@ __device__ __forceinline__ void stage_tiers(const TraceParams& p, uint32_t* s_tw
 #define VF_TRACE_THREADS 128  // block size (A/B: 256 with VF_MINB 4 keeps the 64-register cap)
 #endif
 constexpr unsigned kTraceThreads = VF_TRACE_THREADS;
-template <uint32_t KINDS, bool RESTART, bool COUNT, uint32_t SPEC = 0>
+template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec>
 __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
                                                     uint64_t n, unsigned long long* __restrict__ counters,
@@ -735,7 +854,7 @@ __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const Tra
   Ctr<COUNT> ct;
   ct.touch_map = p.touch;
   if (gid < n) {
-    Lane<KINDS, RESTART, COUNT, SPEC> L;
+    Lane<KINDS, RESTART, COUNT, D> L;
     uint32_t stk[VF_MAX_TIERS];
     int4 out = miss_record();
     if (L.start(p, buf, s_tw, __ldg(rays + 2 * gid), __ldg(rays + 2 * gid + 1), ct)) {
@@ -936,28 +1055,68 @@ KernelFn select_kernel(uint32_t kinds, bool restart, bool count, bool persistent
 #endif
 }
 
-// Compiled-in formats (Lane SPEC): R(A^3) G(M) with a cubic root, no DF — the cfg4 / cfg5 / t512
-// headline formats and their neighbours in the sweeps. Other formats run the generic kernel.
-template <uint32_t SPEC>
+// Compiled-in formats: R(A^3) G(M) (RawSvdag: the cfg4 / cfg5 / t512 headline formats and their
+// sweep neighbours) and the cfg2 / cfg3 headline formats (Packed). Others run the generic kernel.
+template <uint32_t KINDS, class D>
 KernelFn spec_kernel(bool restart) {
-  return restart ? trace_kernel<5, true, false, SPEC> : trace_kernel<5, false, false, SPEC>;
+  return restart ? trace_kernel<KINDS, true, false, D> : trace_kernel<KINDS, false, false, D>;
+}
+
+constexpr LevelSpec kFmtG5R3[] = {{VF_SVDAG, 1, 5}, {VF_RAW, 3, 1}};                     // cfg2
+constexpr LevelSpec kFmtT22T21R4[] = {{VF_NTREE, 2, 2}, {VF_NTREE, 2, 1}, {VF_RAW, 4, 1}};  // cfg3
+constexpr LevelSpec kFmtT21T22R4[] = {{VF_NTREE, 2, 1}, {VF_NTREE, 2, 2}, {VF_RAW, 4, 1}};  // cfg3 (other order)
+constexpr LevelSpec kFmtS5R5[] = {{VF_SVO, 1, 5}, {VF_RAW, 5, 1}};                        // cfg3
+constexpr LevelSpec kFmtG2R2[] = {{VF_SVDAG, 1, 2}, {VF_RAW, 2, 1}};                      // tests
+constexpr LevelSpec kFmtT11T12R1[] = {{VF_NTREE, 1, 1}, {VF_NTREE, 1, 2}, {VF_RAW, 1, 1}};  // tests
+constexpr Packs kPkG5R3 = make_packs(kFmtG5R3), kPkT22T21R4 = make_packs(kFmtT22T21R4),
+                kPkT21T22R4 = make_packs(kFmtT21T22R4), kPkS5R5 = make_packs(kFmtS5R5),
+                kPkG2R2 = make_packs(kFmtG2R2), kPkT11T12R1 = make_packs(kFmtT11T12R1);
+
+template <size_t NL>
+bool same_format(const Format& f, const LevelSpec (&lv)[NL]) {
+  if (f.n_levels != NL) return false;
+  for (size_t l = 0; l < NL; ++l) {
+    const vf_level& v = f.levels[l];
+    if (v.kind != lv[l].kind) return false;
+    if (v.kind == VF_RAW) {
+      if (v.log2_extent[0] != lv[l].lf || v.log2_extent[1] != lv[l].lf || v.log2_extent[2] != lv[l].lf) return false;
+    } else if (v.kind == VF_NTREE) {
+      if (v.log2_fanout != lv[l].lf || v.depth != lv[l].depth) return false;
+    } else if (v.depth != lv[l].depth) {
+      return false;
+    }
+  }
+  return true;
 }
 
 KernelFn select_spec(const Format& f, bool restart) {
 #ifdef VF_ONLY_KINDS
-  if (VF_ONLY_KINDS != 5) return nullptr;
+  constexpr uint32_t K = VF_ONLY_KINDS;
+#define VF_HAS(k) (K == (k))
+#else
+#define VF_HAS(k) true
 #endif
-  if (f.n_levels != 2 || f.levels[0].kind != VF_RAW || f.levels[1].kind != VF_SVDAG) return nullptr;
-  const uint8_t* e = f.levels[0].log2_extent;
-  if (e[0] != e[1] || e[1] != e[2]) return nullptr;
-  switch (((uint32_t)e[0] << 8) | f.levels[1].depth) {
+  if (VF_HAS(5) && f.n_levels == 2 && f.levels[0].kind == VF_RAW && f.levels[1].kind == VF_SVDAG) {
+    const uint8_t* e = f.levels[0].log2_extent;
+    if (e[0] == e[1] && e[1] == e[2]) switch (((uint32_t)e[0] << 8) | f.levels[1].depth) {
 #define VF_SPEC(a, m) \
-  case ((a) << 8) | (m): return spec_kernel<((a) << 8) | (m)>(restart);
-    VF_SPEC(4, 7) VF_SPEC(4, 8) VF_SPEC(3, 8) VF_SPEC(3, 7) VF_SPEC(4, 5) VF_SPEC(2, 7) VF_SPEC(6, 5)
-    VF_SPEC(2, 3) VF_SPEC(1, 4)  // small instances for the parity tests
+  case ((a) << 8) | (m): return spec_kernel<5, RawSvdag<a, m>>(restart);
+        VF_SPEC(4, 7) VF_SPEC(4, 8) VF_SPEC(3, 8) VF_SPEC(3, 7) VF_SPEC(4, 5) VF_SPEC(2, 7) VF_SPEC(6, 5)
+        VF_SPEC(2, 3) VF_SPEC(1, 4)  // small instances for the parity tests
 #undef VF_SPEC
-    default: return nullptr;
+        default: break;
+      }
   }
+#ifndef VF_ONLY_KINDS
+  if (same_format(f, kFmtG5R3)) return spec_kernel<5, VF_PACKED(kPkG5R3)>(restart);
+  if (same_format(f, kFmtG2R2)) return spec_kernel<5, VF_PACKED(kPkG2R2)>(restart);
+  if (same_format(f, kFmtT22T21R4)) return spec_kernel<9, VF_PACKED(kPkT22T21R4)>(restart);
+  if (same_format(f, kFmtT21T22R4)) return spec_kernel<9, VF_PACKED(kPkT21T22R4)>(restart);
+  if (same_format(f, kFmtT11T12R1)) return spec_kernel<9, VF_PACKED(kPkT11T12R1)>(restart);
+  if (same_format(f, kFmtS5R5)) return spec_kernel<3, VF_PACKED(kPkS5R5)>(restart);
+#endif
+#undef VF_HAS
+  return nullptr;
 }
 
 // resident blocks per SM for a persistent kernel (cached per function and device)

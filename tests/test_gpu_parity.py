@@ -373,12 +373,14 @@ def test_payload_rgba_and_entry_face(fmt):
 
 
 # ---------------------------------------------------------------- compiled-in formats (Lane SPEC)
-@pytest.mark.parametrize("fmt,dims", [("R(2^3) G(3)", 32), ("R(1^3) G(4)", 32)])
+@pytest.mark.parametrize("fmt,dims", [("R(2^3) G(3)", 32), ("R(1^3) G(4)", 32), ("G(2) R(2^3)", 16),
+                                      ("T(1, 1) T(1, 2) R(1^3)", 16)])
 @pytest.mark.parametrize("p", [0.02, 0.3])
 def test_compiled_in_format_vs_oracle(fmt, dims, p):
-    """R(A^3) G(M) formats run a kernel with the format compiled in (trace.cu select_spec: tier
-    geometry as arithmetic in the tier index). Same oracle parity as the generic kernel, stack and
-    restart, payload included; the generic kernel (VF_NO_SPEC, subprocess) returns the same bits."""
+    """Formats with a compiled-in kernel (trace.cu select_spec: R(A^3) G(M) as arithmetic in the
+    tier index, other listed formats as packed compile-time tier tables). Same oracle parity as the
+    generic kernel, stack and restart, payload included; the generic kernel (VF_NO_SPEC,
+    subprocess) returns the same bits."""
     import os
     import subprocess
     import sys
