@@ -869,6 +869,9 @@ __global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const Tra
       }
     }
     hits[gid] = out;
+#ifdef VF_RAY_TESTS  // analysis build (tools/ray_tests_dump.py): per-ray cell tests of the counting run
+    if (COUNT) hits[gid].x = (int)ct.v[VF_CTR_CELL_TESTS];
+#endif
     if (p.payload && out.x < 0) p.payload[gid] = make_uint2(0u, 0u);
     ct.add(VF_CTR_RAYS);
   }

@@ -1,3 +1,6 @@
+"""Per-ray cell tests of the counting run (analysis build: tools/build_variant.sh raytests -DVF_RAY_TESTS;
+then VF_LIB=build/variant_raytests/libvf.so python tools/ray_tests_dump.py) -> gpurun_out/raytests_<cfg>.npy,
+the input of the block-compaction simulation in DESIGN.md §11."""
 import sys, os, numpy as np, torch
 sys.path.insert(0, "/root/repo")
 import bench, inputs
