@@ -181,8 +181,9 @@ VF_API vf_status vf_trace_ex(const vf_handle* h, const vf_ray* rays, uint64_t n,
  * device->host and returns when the hits are on the host. Large frames are cut into chunks
  * pipelined over the handle's internal streams (copy-in of chunk i+1, trace of chunk i and
  * copy-out of chunk i-1 overlap); the work is ordered after prior work on cuda_stream.
- * Staging device memory is owned by the handle (grown on demand; calls on one handle must not
- * overlap). Host buffers should be pinned (cudaHostAlloc / torch pin_memory) for overlap. */
+ * Staging device memory is owned by the handle (grown on demand); concurrent calls on one handle
+ * are serialised by a per-handle lock. Host buffers should be pinned (cudaHostAlloc / torch
+ * pin_memory) for overlap. */
 VF_API vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hit* host_hits, uint32_t trace_flags,
                         void* cuda_stream);
 

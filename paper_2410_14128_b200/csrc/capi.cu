@@ -195,6 +195,7 @@ vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hi
     return VF_ERR_INVALID_ARG;
   }
   DeviceGuard g(h->device);
+  std::lock_guard<std::mutex> lock(h->host_mu);  // staging buffer and pipeline streams are per handle
   cudaStream_t s = (cudaStream_t)cuda_stream;
   const size_t rb = n * sizeof(vf_ray), hb = n * sizeof(vf_hit);
   const size_t need = ((rb + 255) & ~(size_t)255) + hb;

@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 #include <string>
 
 #include "../../include/vf.h"
@@ -99,6 +100,7 @@ struct Handle {
   // persistent-trace work counters: kWorkSlots x {next ray, finished blocks}, self-resetting
   unsigned long long* work = nullptr;
   mutable std::atomic<uint32_t> work_slot{0};
+  std::mutex host_mu;  // vf_trace_host: serialises calls on one handle (shared staging and streams)
 };
 
 constexpr uint32_t kWorkSlots = 64;
