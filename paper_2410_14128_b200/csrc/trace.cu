@@ -293,10 +293,10 @@ __device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, ui
 
 // ---- compiled-in formats (the paper's per-format generated code, §4, as template instances) --
 // A format descriptor D gives the tier geometry and flags as functions of the tier index t:
-//   NoSpec        — generic: read from the tier table (any format)
-//   RawSvdag<A,M> — R(A^3) G(M): lc = M - t, 2x2x2 cells below tier 0 (pure arithmetic)
-//   Packed<...>   — any cubic format of <= 8 tiers without DF: per-tier fields packed into
-//                   compile-time immediates (4 bits per tier), extracted with a shift and a mask
+//   NoSpec          — generic: read from the tier table (any format)
+//   RawSvdag<A,M>   — R(A^3) G(M): lc = M - t, 2x2x2 cells below tier 0
+//   SparseRaw<...>  — NS uniform sparse tiers (one kind, one fan-out) over a Raw bottom level
+// (pure arithmetic in t; a packed compile-time table variant measured 2-8 % slower)
 struct NoSpec {
   static constexpr bool kStatic = false;
 };
@@ -317,78 +317,36 @@ struct RawSvdag {
   __device__ static __forceinline__ int level_top(int tu) { return tu == 0 ? 0 : 1; }
 };
 
+// NS sparse tiers of one kind with per-axis fan-out 2^LF each (SVO / SVDAG: LF = 1, N^3: LF = n)
+// over a cubic Raw bottom level R(A^3); bit t of LASTM / TOPM: sparse tier t is the last / first
+// tier of its level. All geometry is arithmetic in t (cfg2 G(5) R(3^3), cfg3 T(2,2) T(2,1) R(4^3)).
+template <uint32_t KIND, uint32_t LF, uint32_t NS, uint32_t A, uint32_t LASTM, uint32_t TOPM>
+struct SparseRaw {
+  static constexpr bool kStatic = true;
+  static constexpr uint32_t LC0 = LF * (NS - 1) + A;  // lc of tier 0
+  __device__ static __forceinline__ uint32_t lc(int t) { return t == (int)NS ? 0u : LC0 - LF * (uint32_t)t; }
+  __device__ static __forceinline__ uint32_t msk(int t) { return t == (int)NS ? (1u << A) - 1u : (1u << LF) - 1u; }
+  __device__ static __forceinline__ uint32_t sx(int t) { return t == (int)NS ? A : LF; }
+  __device__ static __forceinline__ uint32_t sxy(int t) { return t == (int)NS ? 2u * A : 2u * LF; }
+  __device__ static __forceinline__ uint32_t kind(int t) { return t == (int)NS ? (uint32_t)K_RAW : KIND; }
+  __device__ static __forceinline__ bool finest(int t) { return t == (int)NS; }
+  __device__ static __forceinline__ bool last(int t) { return t == (int)NS || ((LASTM >> t) & 1u); }
+  __device__ static __forceinline__ bool top(int t) { return t == (int)NS || ((TOPM >> t) & 1u); }
+  __device__ static __forceinline__ uint32_t lcp(int t) { return t == 0 ? 15u : LC0 + LF - LF * (uint32_t)t; }
+  // deepest tau in [1, NS] with lc(tau - 1) = LF (NS - tau) + A > h; 0 if none
+  __device__ static __forceinline__ int tau(uint32_t h) {
+    if (h < A) return (int)NS;
+    const int tu = (int)NS - 1 - (int)((h - A) / LF);
+    return tu > 0 ? tu : 0;
+  }
+  __device__ static __forceinline__ int level_top(int tu) {
+    return tu == (int)NS ? (int)NS : 31 - __clz(TOPM & ((2u << tu) - 1u));
+  }
+};
+
 struct LevelSpec {
   uint32_t kind, lf, depth;  // VF_RAW / VF_SVO / VF_SVDAG / VF_NTREE, log2 fan-out per axis, tiers
 };
-struct Packs {
-  uint32_t nt, lc, lf, kind, last, top, lcp, ltop, tau_lo, tau_hi;
-};
-// Tier tables of a cubic level list (the same expansion as format.cu, at compile time).
-template <size_t NL>
-constexpr Packs make_packs(const LevelSpec (&lv)[NL]) {
-  uint32_t kind[VF_MAX_TIERS] = {}, lf[VF_MAX_TIERS] = {}, top[VF_MAX_TIERS] = {}, last[VF_MAX_TIERS] = {},
-           ltop[VF_MAX_TIERS] = {}, lc[VF_MAX_TIERS] = {};
-  uint32_t nt = 0, total = 0;
-  for (size_t l = 0; l < NL; ++l) {
-    const uint32_t k = lv[l].kind == VF_RAW ? K_RAW : lv[l].kind == VF_SVO ? K_SVO : lv[l].kind == VF_SVDAG ? K_SVDAG : K_NTREE;
-    const uint32_t f = (lv[l].kind == VF_SVO || lv[l].kind == VF_SVDAG) ? 1u : lv[l].lf;
-    const uint32_t d = lv[l].kind == VF_RAW ? 1u : lv[l].depth;
-    for (uint32_t i = 0; i < d; ++i) {
-      kind[nt] = k;
-      lf[nt] = f;
-      top[nt] = i == 0;
-      last[nt] = i + 1 == d;
-      ltop[nt] = nt - i;
-      total += f;
-      ++nt;
-    }
-  }
-  uint32_t rem = total;
-  for (uint32_t t = 0; t < nt; ++t) {
-    rem -= lf[t];
-    lc[t] = rem;
-  }
-  Packs p{};
-  p.nt = nt;
-  for (uint32_t t = 0; t < nt; ++t) {
-    p.lc |= lc[t] << (4 * t);
-    p.lf |= lf[t] << (4 * t);
-    p.kind |= kind[t] << (4 * t);
-    p.last |= last[t] << t;
-    p.top |= top[t] << t;
-    p.lcp |= (t ? lc[t - 1] : 15u) << (4 * t);
-    p.ltop |= ltop[t] << (4 * t);
-  }
-  for (uint32_t h = 0; h < 16; ++h) {
-    uint32_t tu = 0;
-    for (uint32_t t = 1; t < nt; ++t)
-      if (lc[t - 1] > h) tu = t;
-    if (h < 8)
-      p.tau_lo |= tu << (4 * h);
-    else
-      p.tau_hi |= tu << (4 * (h - 8));
-  }
-  return p;
-}
-
-template <uint32_t NT, uint32_t LC, uint32_t LF, uint32_t KIND, uint32_t LAST, uint32_t TOP, uint32_t LCP,
-          uint32_t LTOP, uint32_t TAU_LO, uint32_t TAU_HI>
-struct Packed {
-  static constexpr bool kStatic = true;
-  __device__ static __forceinline__ uint32_t f4(uint32_t pack, int t) { return (pack >> (4 * t)) & 15u; }
-  __device__ static __forceinline__ uint32_t lc(int t) { return f4(LC, t); }
-  __device__ static __forceinline__ uint32_t msk(int t) { return (1u << f4(LF, t)) - 1u; }
-  __device__ static __forceinline__ uint32_t sx(int t) { return f4(LF, t); }
-  __device__ static __forceinline__ uint32_t sxy(int t) { return 2u * f4(LF, t); }
-  __device__ static __forceinline__ uint32_t kind(int t) { return f4(KIND, t); }
-  __device__ static __forceinline__ bool finest(int t) { return t == (int)NT - 1; }
-  __device__ static __forceinline__ bool last(int t) { return (LAST >> t) & 1u; }
-  __device__ static __forceinline__ bool top(int t) { return (TOP >> t) & 1u; }
-  __device__ static __forceinline__ uint32_t lcp(int t) { return f4(LCP, t); }
-  __device__ static __forceinline__ int tau(uint32_t h) { return (int)(h < 8 ? f4(TAU_LO, h) : f4(TAU_HI, h - 8)); }
-  __device__ static __forceinline__ int level_top(int tu) { return (int)f4(LTOP, tu); }
-};
-#define VF_PACKED(P) Packed<P.nt, P.lc, P.lf, P.kind, P.last, P.top, P.lcp, P.ltop, P.tau_lo, P.tau_hi>
 
 enum { IT_CONTINUE = 0, IT_HIT = 1, IT_MISS = 2 };
 
@@ -1059,7 +1017,7 @@ KernelFn select_kernel(uint32_t kinds, bool restart, bool count, bool persistent
 }
 
 // Compiled-in formats: R(A^3) G(M) (RawSvdag: the cfg4 / cfg5 / t512 headline formats and their
-// sweep neighbours) and the cfg2 / cfg3 headline formats (Packed). Others run the generic kernel.
+// sweep neighbours) and the cfg2 / cfg3 headline formats (SparseRaw). Others run the generic kernel.
 template <uint32_t KINDS, class D>
 KernelFn spec_kernel(bool restart) {
   return restart ? trace_kernel<KINDS, true, false, D> : trace_kernel<KINDS, false, false, D>;
@@ -1071,9 +1029,6 @@ constexpr LevelSpec kFmtT21T22R4[] = {{VF_NTREE, 2, 1}, {VF_NTREE, 2, 2}, {VF_RA
 constexpr LevelSpec kFmtS5R5[] = {{VF_SVO, 1, 5}, {VF_RAW, 5, 1}};                        // cfg3
 constexpr LevelSpec kFmtG2R2[] = {{VF_SVDAG, 1, 2}, {VF_RAW, 2, 1}};                      // tests
 constexpr LevelSpec kFmtT11T12R1[] = {{VF_NTREE, 1, 1}, {VF_NTREE, 1, 2}, {VF_RAW, 1, 1}};  // tests
-constexpr Packs kPkG5R3 = make_packs(kFmtG5R3), kPkT22T21R4 = make_packs(kFmtT22T21R4),
-                kPkT21T22R4 = make_packs(kFmtT21T22R4), kPkS5R5 = make_packs(kFmtS5R5),
-                kPkG2R2 = make_packs(kFmtG2R2), kPkT11T12R1 = make_packs(kFmtT11T12R1);
 
 template <size_t NL>
 bool same_format(const Format& f, const LevelSpec (&lv)[NL]) {
@@ -1111,12 +1066,12 @@ KernelFn select_spec(const Format& f, bool restart) {
       }
   }
 #ifndef VF_ONLY_KINDS
-  if (same_format(f, kFmtG5R3)) return spec_kernel<5, VF_PACKED(kPkG5R3)>(restart);
-  if (same_format(f, kFmtG2R2)) return spec_kernel<5, VF_PACKED(kPkG2R2)>(restart);
-  if (same_format(f, kFmtT22T21R4)) return spec_kernel<9, VF_PACKED(kPkT22T21R4)>(restart);
-  if (same_format(f, kFmtT21T22R4)) return spec_kernel<9, VF_PACKED(kPkT21T22R4)>(restart);
-  if (same_format(f, kFmtT11T12R1)) return spec_kernel<9, VF_PACKED(kPkT11T12R1)>(restart);
-  if (same_format(f, kFmtS5R5)) return spec_kernel<3, VF_PACKED(kPkS5R5)>(restart);
+  if (same_format(f, kFmtG5R3)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 3, 0x10, 0x1>>(restart);
+  if (same_format(f, kFmtG2R2)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 2, 2, 0x2, 0x1>>(restart);
+  if (same_format(f, kFmtT22T21R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x6, 0x5>>(restart);
+  if (same_format(f, kFmtT21T22R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x5, 0x3>>(restart);
+  if (same_format(f, kFmtT11T12R1)) return spec_kernel<9, SparseRaw<K_NTREE, 1, 3, 1, 0x5, 0x3>>(restart);
+  if (same_format(f, kFmtS5R5)) return spec_kernel<3, SparseRaw<K_SVO, 1, 5, 5, 0x10, 0x1>>(restart);
 #endif
 #undef VF_HAS
   return nullptr;
