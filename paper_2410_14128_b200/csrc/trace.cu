@@ -294,28 +294,40 @@ __device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, ui
 // ---- compiled-in formats (the paper's per-format generated code, §4, as template instances) --
 // A format descriptor D gives the tier geometry and flags as functions of the tier index t:
 //   NoSpec          — generic: read from the tier table (any format)
-//   RawSvdag<A,M>   — R(A^3) G(M): lc = M - t, 2x2x2 cells below tier 0
+//   TopSparse<...>  — optional Raw top over one uniform sparse level: R(A^3) G(M), G(L), T(n,d), ...
 //   SparseRaw<...>  — NS uniform sparse tiers (one kind, one fan-out) over a Raw bottom level
 // (pure arithmetic in t; a packed compile-time table variant measured 2-8 % slower)
 struct NoSpec {
   static constexpr bool kStatic = false;
 };
 
-template <uint32_t A, uint32_t M>
-struct RawSvdag {
+// An optional cubic Raw top level R(A^3) (A = 0: none) over one sparse level of NS tiers of one
+// kind with per-axis fan-out 2^LF each (SVO / SVDAG: LF = 1, N^3: LF = n): R(A^3) G(M), G(L),
+// S(L), T(n, d), R(A^3) T(n, d), ... lc = LF (NS + off - 1 - t), off = (A > 0).
+template <uint32_t A, uint32_t KIND, uint32_t LF, uint32_t NS>
+struct TopSparse {
   static constexpr bool kStatic = true;
-  __device__ static __forceinline__ uint32_t lc(int t) { return M - (uint32_t)t; }
-  __device__ static __forceinline__ uint32_t msk(int t) { return t == 0 ? (1u << A) - 1u : 1u; }
-  __device__ static __forceinline__ uint32_t sx(int t) { return t == 0 ? A : 1u; }
-  __device__ static __forceinline__ uint32_t sxy(int t) { return t == 0 ? 2u * A : 2u; }
-  __device__ static __forceinline__ uint32_t kind(int t) { return t == 0 ? (uint32_t)K_RAW : (uint32_t)K_SVDAG; }
-  __device__ static __forceinline__ bool finest(int t) { return t == (int)M; }
-  __device__ static __forceinline__ bool last(int t) { return t == 0 || t == (int)M; }
-  __device__ static __forceinline__ bool top(int t) { return t <= 1; }
-  __device__ static __forceinline__ uint32_t lcp(int t) { return t == 0 ? 15u : M + 1u - (uint32_t)t; }
-  __device__ static __forceinline__ int tau(uint32_t h) { return h >= M ? 0 : (int)(M - h); }
-  __device__ static __forceinline__ int level_top(int tu) { return tu == 0 ? 0 : 1; }
+  static constexpr int OFF = A > 0 ? 1 : 0;
+  static constexpr int NT = (int)NS + OFF;
+  __device__ static __forceinline__ bool raw(int t) { return A > 0 && t == 0; }
+  __device__ static __forceinline__ uint32_t lc(int t) { return LF * (uint32_t)(NT - 1 - t); }
+  __device__ static __forceinline__ uint32_t msk(int t) { return raw(t) ? (1u << A) - 1u : (1u << LF) - 1u; }
+  __device__ static __forceinline__ uint32_t sx(int t) { return raw(t) ? A : LF; }
+  __device__ static __forceinline__ uint32_t sxy(int t) { return raw(t) ? 2u * A : 2u * LF; }
+  __device__ static __forceinline__ uint32_t kind(int t) { return raw(t) ? (uint32_t)K_RAW : KIND; }
+  __device__ static __forceinline__ bool finest(int t) { return t == NT - 1; }
+  __device__ static __forceinline__ bool last(int t) { return raw(t) || t == NT - 1; }
+  __device__ static __forceinline__ bool top(int t) { return t <= OFF; }
+  __device__ static __forceinline__ uint32_t lcp(int t) { return t == 0 ? 15u : LF * (uint32_t)(NT - t); }
+  // deepest tau in [1, NT - 1] with lc(tau - 1) = LF (NT - tau) > h; 0 if none
+  __device__ static __forceinline__ int tau(uint32_t h) {
+    const int tu = NT - 1 - (int)(h / LF);
+    return tu > 0 ? tu : 0;
+  }
+  __device__ static __forceinline__ int level_top(int tu) { return tu == 0 ? 0 : OFF; }
 };
+template <uint32_t A, uint32_t M>
+using RawSvdag = TopSparse<A, K_SVDAG, 1, M>;
 
 // NS sparse tiers of one kind with per-axis fan-out 2^LF each (SVO / SVDAG: LF = 1, N^3: LF = n)
 // over a cubic Raw bottom level R(A^3); bit t of LASTM / TOPM: sparse tier t is the last / first
@@ -343,6 +355,8 @@ struct SparseRaw {
     return tu == (int)NS ? (int)NS : 31 - __clz(TOPM & ((2u << tu) - 1u));
   }
 };
+
+constexpr uint32_t K_OF_VF_SVO = K_SVO, K_OF_VF_SVDAG = K_SVDAG, K_OF_VF_NTREE = K_NTREE;
 
 struct LevelSpec {
   uint32_t kind, lf, depth;  // VF_RAW / VF_SVO / VF_SVDAG / VF_NTREE, log2 fan-out per axis, tiers
@@ -1065,6 +1079,32 @@ KernelFn select_spec(const Format& f, bool restart) {
         default: break;
       }
   }
+#ifndef VF_ONLY_KINDS
+  // single sparse levels and Raw-topped sparse levels of the sweeps
+  if (f.n_levels == 1 || (f.n_levels == 2 && f.levels[0].kind == VF_RAW)) {
+    const vf_level& sp = f.levels[f.n_levels - 1];
+    uint32_t a = 0;
+    if (f.n_levels == 2) {
+      const uint8_t* e = f.levels[0].log2_extent;
+      if (e[0] != e[1] || e[1] != e[2]) return nullptr;
+      a = e[0];
+    }
+    const uint32_t lf = sp.kind == VF_NTREE ? sp.log2_fanout : 1u;
+    const uint32_t key = (a << 24) | (sp.kind << 16) | (lf << 8) | sp.depth;
+    switch (key) {
+#define VF_TS(a, k, lf, ns, kinds) \
+  case ((a) << 24) | ((k) << 16) | ((lf) << 8) | (ns): return spec_kernel<kinds, TopSparse<a, K_OF_##k, lf, ns>>(restart);
+      VF_TS(0, VF_SVDAG, 1, 11, 4) VF_TS(0, VF_SVO, 1, 11, 2) VF_TS(0, VF_SVDAG, 1, 8, 4) VF_TS(0, VF_SVO, 1, 8, 2)
+      VF_TS(0, VF_SVDAG, 1, 10, 4) VF_TS(0, VF_SVO, 1, 10, 2) VF_TS(0, VF_SVDAG, 1, 12, 4) VF_TS(0, VF_SVO, 1, 12, 2)
+      VF_TS(0, VF_SVDAG, 1, 9, 4) VF_TS(0, VF_SVO, 1, 9, 2)
+      VF_TS(4, VF_SVO, 1, 7, 3) VF_TS(6, VF_SVO, 1, 5, 3) VF_TS(4, VF_SVO, 1, 5, 3)
+      VF_TS(0, VF_NTREE, 2, 4, 8) VF_TS(0, VF_NTREE, 2, 5, 8) VF_TS(0, VF_NTREE, 2, 6, 8) VF_TS(1, VF_NTREE, 2, 5, 9)
+      VF_TS(0, VF_SVDAG, 1, 4, 4) VF_TS(0, VF_NTREE, 1, 4, 8) VF_TS(2, VF_NTREE, 1, 3, 9)  // tests
+#undef VF_TS
+      default: break;
+    }
+  }
+#endif
 #ifndef VF_ONLY_KINDS
   if (same_format(f, kFmtG5R3)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 3, 0x10, 0x1>>(restart);
   if (same_format(f, kFmtG2R2)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 2, 2, 0x2, 0x1>>(restart);
