@@ -329,6 +329,31 @@ struct TopSparse {
 template <uint32_t A, uint32_t M>
 using RawSvdag = TopSparse<A, K_SVDAG, 1, M>;
 
+// An optional cubic Raw top R(A^3) over two octree levels (SVO / SVDAG) of N1 then N2 tiers:
+// S(a) G(b), R(A^3) S(a) G(b), ... — uniform 2x2x2 tiers below the top, lc = NT - 1 - t.
+template <uint32_t A, uint32_t K1, uint32_t N1, uint32_t K2, uint32_t N2>
+struct TwoSparse {
+  static constexpr bool kStatic = true;
+  static constexpr int OFF = A > 0 ? 1 : 0;
+  static constexpr int B = OFF + (int)N1;  // first tier of the second sparse level
+  static constexpr int NT = B + (int)N2;
+  __device__ static __forceinline__ bool raw(int t) { return A > 0 && t == 0; }
+  __device__ static __forceinline__ uint32_t lc(int t) { return (uint32_t)(NT - 1 - t); }
+  __device__ static __forceinline__ uint32_t msk(int t) { return raw(t) ? (1u << A) - 1u : 1u; }
+  __device__ static __forceinline__ uint32_t sx(int t) { return raw(t) ? A : 1u; }
+  __device__ static __forceinline__ uint32_t sxy(int t) { return raw(t) ? 2u * A : 2u; }
+  __device__ static __forceinline__ uint32_t kind(int t) { return raw(t) ? (uint32_t)K_RAW : (t < B ? K1 : K2); }
+  __device__ static __forceinline__ bool finest(int t) { return t == NT - 1; }
+  __device__ static __forceinline__ bool last(int t) { return raw(t) || t == B - 1 || t == NT - 1; }
+  __device__ static __forceinline__ bool top(int t) { return t <= OFF || t == B; }
+  __device__ static __forceinline__ uint32_t lcp(int t) { return t == 0 ? 15u : (uint32_t)(NT - t); }
+  __device__ static __forceinline__ int tau(uint32_t h) {
+    const int tu = NT - 1 - (int)h;
+    return tu > 0 ? tu : 0;
+  }
+  __device__ static __forceinline__ int level_top(int tu) { return tu == 0 ? 0 : (tu < B ? OFF : B); }
+};
+
 // NS sparse tiers of one kind with per-axis fan-out 2^LF each (SVO / SVDAG: LF = 1, N^3: LF = n)
 // over a cubic Raw bottom level R(A^3); bit t of LASTM / TOPM: sparse tier t is the last / first
 // tier of its level. All geometry is arithmetic in t (cfg2 G(5) R(3^3), cfg3 T(2,2) T(2,1) R(4^3)).
@@ -1106,6 +1131,28 @@ KernelFn select_spec(const Format& f, bool restart) {
   }
 #endif
 #ifndef VF_ONLY_KINDS
+  if (f.n_levels == 2 || f.n_levels == 3) {  // [R(A^3)] S|G(a) S|G(b)
+    const uint32_t o = f.n_levels == 3 ? 1u : 0u;
+    const vf_level &l1 = f.levels[o], &l2 = f.levels[o + 1];
+    const bool oct1 = l1.kind == VF_SVO || l1.kind == VF_SVDAG, oct2 = l2.kind == VF_SVO || l2.kind == VF_SVDAG;
+    uint32_t a = 0;
+    bool ok = oct1 && oct2;
+    if (ok && o) {
+      const uint8_t* e = f.levels[0].log2_extent;
+      ok = f.levels[0].kind == VF_RAW && e[0] == e[1] && e[1] == e[2];
+      a = e[0];
+    }
+    if (ok) switch ((a << 24) | (l1.kind << 20) | ((uint32_t)l1.depth << 12) | (l2.kind << 8) | l2.depth) {
+#define VF_2S(a, k1, n1, k2, n2, kinds) \
+  case ((a) << 24) | ((k1) << 20) | ((n1) << 12) | ((k2) << 8) | (n2): \
+    return spec_kernel<kinds, TwoSparse<a, K_OF_##k1, n1, K_OF_##k2, n2>>(restart);
+        VF_2S(0, VF_SVO, 3, VF_SVDAG, 8, 6) VF_2S(0, VF_SVO, 5, VF_SVDAG, 6, 6) VF_2S(0, VF_SVO, 7, VF_SVDAG, 4, 6)
+        VF_2S(4, VF_SVO, 3, VF_SVDAG, 4, 7)
+        VF_2S(0, VF_SVO, 2, VF_SVDAG, 2, 6) VF_2S(1, VF_SVDAG, 1, VF_SVO, 2, 7)  // tests
+#undef VF_2S
+        default: break;
+      }
+  }
   if (same_format(f, kFmtG5R3)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 3, 0x10, 0x1>>(restart);
   if (same_format(f, kFmtG2R2)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 2, 2, 0x2, 0x1>>(restart);
   if (same_format(f, kFmtT22T21R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x6, 0x5>>(restart);
