@@ -304,9 +304,11 @@ struct NoSpec {
 // An optional cubic Raw top level R(A^3) (A = 0: none) over one sparse level of NS tiers of one
 // kind with per-axis fan-out 2^LF each (SVO / SVDAG: LF = 1, N^3: LF = n): R(A^3) G(M), G(L),
 // S(L), T(n, d), R(A^3) T(n, d), ... lc = LF (NS + off - 1 - t), off = (A > 0).
-template <uint32_t A, uint32_t KIND, uint32_t LF, uint32_t NS>
+template <uint32_t A, uint32_t KIND, uint32_t LF, uint32_t NS, bool DFTOP = false>
 struct TopSparse {
   static constexpr bool kStatic = true;
+  // DFTOP: the top level is a DF grid D(A^3, M) (2-word cells {TermInt, L1 distance})
+  __device__ static __forceinline__ bool df(int t) { return DFTOP && A > 0 && t == 0; }
   static constexpr int OFF = A > 0 ? 1 : 0;
   static constexpr int NT = (int)NS + OFF;
   __device__ static __forceinline__ bool raw(int t) { return A > 0 && t == 0; }
@@ -334,6 +336,7 @@ using RawSvdag = TopSparse<A, K_SVDAG, 1, M>;
 template <uint32_t A, uint32_t K1, uint32_t N1, uint32_t K2, uint32_t N2>
 struct TwoSparse {
   static constexpr bool kStatic = true;
+  __device__ static __forceinline__ bool df(int) { return false; }
   static constexpr int OFF = A > 0 ? 1 : 0;
   static constexpr int B = OFF + (int)N1;  // first tier of the second sparse level
   static constexpr int NT = B + (int)N2;
@@ -360,6 +363,7 @@ struct TwoSparse {
 template <uint32_t KIND, uint32_t LF, uint32_t NS, uint32_t A, uint32_t LASTM, uint32_t TOPM>
 struct SparseRaw {
   static constexpr bool kStatic = true;
+  __device__ static __forceinline__ bool df(int) { return false; }
   static constexpr uint32_t LC0 = LF * (NS - 1) + A;  // lc of tier 0
   __device__ static __forceinline__ uint32_t lc(int t) { return t == (int)NS ? 0u : LC0 - LF * (uint32_t)t; }
   __device__ static __forceinline__ uint32_t msk(int t) { return t == (int)NS ? (1u << A) - 1u : (1u << LF) - 1u; }
@@ -437,7 +441,7 @@ struct Lane {
     if constexpr (SPEC) return D::last(t); else return (tw & TW_LAST) != 0;
   }
   __device__ __forceinline__ bool is_df() const {
-    if constexpr (SPEC) return false; else return (tw & TW_DF) != 0;
+    if constexpr (SPEC) return D::df(t); else return (tw & TW_DF) != 0;
   }
   __device__ __forceinline__ bool is_top() const {
     if constexpr (SPEC) return D::top(t); else return (tw & TW_TOP) != 0;
@@ -1106,19 +1110,26 @@ KernelFn select_spec(const Format& f, bool restart) {
   }
 #ifndef VF_ONLY_KINDS
   // single sparse levels and Raw-topped sparse levels of the sweeps
-  if (f.n_levels == 1 || (f.n_levels == 2 && f.levels[0].kind == VF_RAW)) {
+  if (f.n_levels == 1 || (f.n_levels == 2 && (f.levels[0].kind == VF_RAW || f.levels[0].kind == VF_DF))) {
     const vf_level& sp = f.levels[f.n_levels - 1];
     uint32_t a = 0;
+    const uint32_t df = f.n_levels == 2 && f.levels[0].kind == VF_DF;
     if (f.n_levels == 2) {
       const uint8_t* e = f.levels[0].log2_extent;
       if (e[0] != e[1] || e[1] != e[2]) return nullptr;
       a = e[0];
     }
     const uint32_t lf = sp.kind == VF_NTREE ? sp.log2_fanout : 1u;
-    const uint32_t key = (a << 24) | (sp.kind << 16) | (lf << 8) | sp.depth;
+    const uint32_t key = (df << 28) | (a << 24) | (sp.kind << 16) | (lf << 8) | sp.depth;
     switch (key) {
 #define VF_TS(a, k, lf, ns, kinds) \
   case ((a) << 24) | ((k) << 16) | ((lf) << 8) | (ns): return spec_kernel<kinds, TopSparse<a, K_OF_##k, lf, ns>>(restart);
+#define VF_DS(a, k, ns) /* DF top D(a^3, M) */ \
+  case (1u << 28) | ((a) << 24) | ((k) << 16) | (1u << 8) | (ns): \
+    return spec_kernel<(1u << K_RAW) | (1u << K_OF_##k), TopSparse<a, K_OF_##k, 1, ns, true>>(restart);
+      VF_DS(4, VF_SVDAG, 7) VF_DS(6, VF_SVDAG, 5) VF_DS(4, VF_SVO, 7) VF_DS(6, VF_SVO, 5) VF_DS(4, VF_SVDAG, 5)
+      VF_DS(4, VF_SVO, 5) VF_DS(2, VF_SVDAG, 2)
+#undef VF_DS
       VF_TS(0, VF_SVDAG, 1, 11, 4) VF_TS(0, VF_SVO, 1, 11, 2) VF_TS(0, VF_SVDAG, 1, 8, 4) VF_TS(0, VF_SVO, 1, 8, 2)
       VF_TS(0, VF_SVDAG, 1, 10, 4) VF_TS(0, VF_SVO, 1, 10, 2) VF_TS(0, VF_SVDAG, 1, 12, 4) VF_TS(0, VF_SVO, 1, 12, 2)
       VF_TS(0, VF_SVDAG, 1, 9, 4) VF_TS(0, VF_SVO, 1, 9, 2)
