@@ -1070,6 +1070,11 @@ constexpr LevelSpec kFmtG5R3[] = {{VF_SVDAG, 1, 5}, {VF_RAW, 3, 1}};            
 constexpr LevelSpec kFmtT22T21R4[] = {{VF_NTREE, 2, 2}, {VF_NTREE, 2, 1}, {VF_RAW, 4, 1}};  // cfg3
 constexpr LevelSpec kFmtT21T22R4[] = {{VF_NTREE, 2, 1}, {VF_NTREE, 2, 2}, {VF_RAW, 4, 1}};  // cfg3 (other order)
 constexpr LevelSpec kFmtS5R5[] = {{VF_SVO, 1, 5}, {VF_RAW, 5, 1}};                        // cfg3
+constexpr LevelSpec kFmtT24R3[] = {{VF_NTREE, 2, 4}, {VF_RAW, 3, 1}};                     // cfg4 sweep
+constexpr LevelSpec kFmtT22T22R3[] = {{VF_NTREE, 2, 2}, {VF_NTREE, 2, 2}, {VF_RAW, 3, 1}};  // cfg4 sweep
+constexpr LevelSpec kFmtT23R5[] = {{VF_NTREE, 2, 3}, {VF_RAW, 5, 1}};                     // cfg4 sweep
+constexpr LevelSpec kFmtS5R4[] = {{VF_SVO, 1, 5}, {VF_RAW, 4, 1}};                        // t512
+constexpr LevelSpec kFmtG5R4[] = {{VF_SVDAG, 1, 5}, {VF_RAW, 4, 1}};                      // t512
 constexpr LevelSpec kFmtG2R2[] = {{VF_SVDAG, 1, 2}, {VF_RAW, 2, 1}};                      // tests
 constexpr LevelSpec kFmtT11T12R1[] = {{VF_NTREE, 1, 1}, {VF_NTREE, 1, 2}, {VF_RAW, 1, 1}};  // tests
 
@@ -1103,6 +1108,7 @@ KernelFn select_spec(const Format& f, bool restart) {
 #define VF_SPEC(a, m) \
   case ((a) << 8) | (m): return spec_kernel<5, RawSvdag<a, m>>(restart);
         VF_SPEC(4, 7) VF_SPEC(4, 8) VF_SPEC(3, 8) VF_SPEC(3, 7) VF_SPEC(4, 5) VF_SPEC(2, 7) VF_SPEC(6, 5)
+        VF_SPEC(8, 3) VF_SPEC(3, 5) VF_SPEC(3, 9) VF_SPEC(7, 2)
         VF_SPEC(2, 3) VF_SPEC(1, 4)  // small instances for the parity tests
 #undef VF_SPEC
         default: break;
@@ -1135,6 +1141,7 @@ KernelFn select_spec(const Format& f, bool restart) {
       VF_TS(0, VF_SVDAG, 1, 9, 4) VF_TS(0, VF_SVO, 1, 9, 2)
       VF_TS(4, VF_SVO, 1, 7, 3) VF_TS(6, VF_SVO, 1, 5, 3) VF_TS(4, VF_SVO, 1, 5, 3)
       VF_TS(0, VF_NTREE, 2, 4, 8) VF_TS(0, VF_NTREE, 2, 5, 8) VF_TS(0, VF_NTREE, 2, 6, 8) VF_TS(1, VF_NTREE, 2, 5, 9)
+      VF_TS(4, VF_NTREE, 2, 4, 9)
       VF_TS(0, VF_SVDAG, 1, 4, 4) VF_TS(0, VF_NTREE, 1, 4, 8) VF_TS(2, VF_NTREE, 1, 3, 9)  // tests
 #undef VF_TS
       default: break;
@@ -1170,6 +1177,11 @@ KernelFn select_spec(const Format& f, bool restart) {
   if (same_format(f, kFmtT21T22R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x5, 0x3>>(restart);
   if (same_format(f, kFmtT11T12R1)) return spec_kernel<9, SparseRaw<K_NTREE, 1, 3, 1, 0x5, 0x3>>(restart);
   if (same_format(f, kFmtS5R5)) return spec_kernel<3, SparseRaw<K_SVO, 1, 5, 5, 0x10, 0x1>>(restart);
+  if (same_format(f, kFmtT24R3)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 4, 3, 0x8, 0x1>>(restart);
+  if (same_format(f, kFmtT22T22R3)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 4, 3, 0xA, 0x5>>(restart);
+  if (same_format(f, kFmtT23R5)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 5, 0x4, 0x1>>(restart);
+  if (same_format(f, kFmtS5R4)) return spec_kernel<3, SparseRaw<K_SVO, 1, 5, 4, 0x10, 0x1>>(restart);
+  if (same_format(f, kFmtG5R4)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 4, 0x10, 0x1>>(restart);
 #endif
 #undef VF_HAS
   return nullptr;
