@@ -157,7 +157,11 @@ enum {
 
 /* Trace n rays (device array) into hits (device array), one thread per ray, asynchronously
  * on cuda_stream; hits are valid after the stream synchronises. Concurrent traces on one
- * handle are allowed (read-only). n = 0 is a no-op. */
+ * handle are allowed (read-only). n = 0 is a no-op. Formats of the library's compiled-in list
+ * (the paper's per-format generated code: R(A^3) G(M), G(L), S(L), T(n,d),
+ * S(a) G(b), D(A^3,M) over S/G, the cfg2/cfg3 headline formats, single Raw grids) run a kernel
+ * with the format's tier geometry compiled in; all others the generic tier-table kernel.
+ * Results are identical (environment VF_NO_SPEC=1 forces the generic kernel). */
 VF_API vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t trace_flags,
                    void* cuda_stream);
 

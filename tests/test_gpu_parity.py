@@ -376,7 +376,7 @@ def test_payload_rgba_and_entry_face(fmt):
 @pytest.mark.parametrize("fmt,dims", [("R(2^3) G(3)", 32), ("R(1^3) G(4)", 32), ("G(2) R(2^3)", 16),
                                       ("T(1, 1) T(1, 2) R(1^3)", 16), ("G(4)", 16), ("T(1, 4)", 16),
                                       ("R(2^3) T(1, 3)", 32), ("S(2) G(2)", 16), ("R(1^3) G(1) S(2)", 16),
-                                      ("D(2^3, 3) G(2)", 16)])
+                                      ("D(2^3, 3) G(2)", 16), ("R(4^3)", 16), ("D(4^3, 3)", 16)])
 @pytest.mark.parametrize("p", [0.02, 0.3])
 def test_compiled_in_format_vs_oracle(fmt, dims, p):
     """Formats with a compiled-in kernel (trace.cu select_spec: R(A^3) G(M) as arithmetic in the
