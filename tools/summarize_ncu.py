@@ -37,9 +37,10 @@ def f(name):
 
 
 rd, wr = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 unit_r = (R.get("dram__bytes_read.sum") or ("", ""))[1]
-scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
-dram = (rd + wr) * scale
+unit_w = (R.get("dram__bytes_write.sum") or ("", ""))[1]
+dram = rd * SCALE.get(unit_r, 1) + wr * SCALE.get(unit_w, 1)  # (read and write may differ in unit)
 print(f"# ncu summary — {label}\n")
 print(f"kernel: `{kname}`\n")
 print("| metric | value |\n|---|---|")
