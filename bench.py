@@ -180,10 +180,19 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # --force-dist (test aid): run the N > 1 code path (NCCL group, chunked trace/gather pipeline,
+    # max-over-ranks reductions) with a single rank
+    dist_on = world > 1 or args.force_dist
+    if dist_on and world == 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    if dist_on:
+        # bind the NCCL communicator to this rank's GPU up front (barriers / collectives use it)
+        dist.init_process_group("nccl", device_id=dev)
     import inputs
     from paper_2410_14128_b200 import vf
 
@@ -237,7 +246,7 @@ def run_ours(args):
     # lasts at least as long as its slowest ray, so chunks much smaller than that cost more in
     # launch tails than the overlap with the gather returns
     k_chunks = args.gather_chunks if args.gather_chunks > 0 else max(1, min(4, max(counts) // (1 << 19)))
-    pipe = shard.ChunkedGather(counts, k_chunks, dev) if world > 1 else None
+    pipe = shard.ChunkedGather(counts, k_chunks, dev) if dist_on else None
     if pipe is not None:
         hits = pipe.hits
 
@@ -254,7 +263,7 @@ def run_ours(args):
         step()
         gather()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -274,13 +283,13 @@ def run_ours(args):
         ends[i].record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     kern_ms = [s.elapsed_time(e) for s, e in zip(kstarts, kends)]
     tot_ms = sum(step_ms)
-    if world > 1:
+    if dist_on:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
@@ -288,7 +297,7 @@ def run_ours(args):
     value = n_total * args.steps / (tot_ms / 1e3) / 1e6
 
     trace_only = None
-    if world > 1:
+    if dist_on:
         # trace-only aggregate (reported beside the end-to-end frame incl. the gather):
         # the same K frames, one launch over the rank's rays, no collective; max over ranks
         tr_ms = []
@@ -317,12 +326,12 @@ def run_ours(args):
     for _ in range(max(3, min(args.steps, 10))):
         flush.fill_(1)
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         t1 = time.perf_counter()
         handle.trace_host(hr, hh, restart=args.restart, incoherent=incoh)
         dt = time.perf_counter() - t1
-        if world > 1:
+        if dist_on:
             t = torch.tensor([dt], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
@@ -406,7 +415,7 @@ def run_ours(args):
         }
         if not args.no_sweep and world == 1 and cfg in SWEEP:
             result["sweep"] = sweep(cfg, vol, rays, hits, stream, flush, args, ref_idx, ref)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
     return result
 
@@ -547,6 +556,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--gather-chunks", type=int, default=0, help="N>1: trace/gather pipeline depth (0: auto)")
+    ap.add_argument("--force-dist", action="store_true", help="test aid: the N>1 code path with one rank")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

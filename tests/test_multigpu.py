@@ -6,6 +6,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch.multiprocessing as mp
 
 from inputs import rays as R
@@ -134,3 +135,40 @@ def test_chunk_bounds_cover_padded_rows():
         assert b[0][0] == 0 and b[-1][1] == max(counts)
         assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
         assert all(hi > lo for lo, hi in b)
+
+
+def _nccl_worker(port, q):
+    import torch
+    import torch.distributed as dist
+    import inputs
+    from paper_2410_14128_b200 import shard, vf
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)  # as bench.py does
+    d = inputs.menger(128, 4)
+    keys, rgba = inputs.voxels_device(d)
+    h = vf.build((keys, rgba, (128, 128, 128)), "G(4) R(3^3)")
+    rays_np, perm = R.perspective(64, 48, 60.0, (-40.3, 60.7, -70.1), (40.5, 40.5, 40.5))
+    rays = torch.from_numpy(rays_np).to(dev)
+    ref = h.trace(rays).cpu().numpy()
+    counts = shard.shard_counts(perm, 64, 1)
+    pipe = shard.ChunkedGather(counts, 3, dev)  # NCCL gather to self, chunk by chunk, async
+    bufs = pipe.run(lambda lo, hi, hv: h.trace(rays[lo:hi], hv))
+    torch.cuda.synchronize()
+    q.put(bool((bufs[0].cpu().numpy() == ref).all()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_chunked_gather_over_nccl_single_rank():
+    """The bench's N>1 pipeline (trace chunk k, async NCCL gather of chunk k) run for real over NCCL
+    with one rank on the box's GPU: the gathered hits equal one whole-frame trace."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    ok = q.get(timeout=300)
+    p.join(60)
+    assert p.exitcode == 0 and ok
