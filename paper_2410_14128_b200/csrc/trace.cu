@@ -876,12 +876,15 @@ __device__ __forceinline__ void stage_tiers(const TraceParams& p, uint32_t* s_tw
 #ifndef VF_MINB
 #define VF_MINB 8  // __launch_bounds__ min blocks per SM (register cap), A/B-tuned
 #endif
+#ifndef VF_MINB_SPEC
+#define VF_MINB_SPEC 9  // compiled-in formats: 56 registers, 9 blocks per SM (A/B: +1.4-2.2 % over 8)
+#endif
 #ifndef VF_TRACE_THREADS
 #define VF_TRACE_THREADS 128  // block size (A/B: 256 with VF_MINB 4 keeps the 64-register cap)
 #endif
 constexpr unsigned kTraceThreads = VF_TRACE_THREADS;
 template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec>
-__global__ void __launch_bounds__(kTraceThreads, VF_MINB) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
+__global__ void __launch_bounds__(kTraceThreads, D::kStatic ? VF_MINB_SPEC : VF_MINB) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
                                                     uint64_t n, unsigned long long* __restrict__ counters,
                                                     unsigned long long* __restrict__ work) {
