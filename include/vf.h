@@ -17,8 +17,10 @@
  *     p(t) = o + t d over [tmin, tmax); plane crossings with equal exact t step together.
  *     Exactness (bit-exact x,y,z and miss flag; t within 1e-4 relative) is guaranteed for
  *     rays in the canonical domain: R <= 4096 per axis; |o_a| in {0} U [2^-16, 2^20);
- *     |d_a| in {0} U [2^-30, 2], d != 0; 0 <= tmin < tmax; tmin and finite tmax in
- *     {0} U [2^-16, 2^20); tmax = +inf allowed. Rays outside it are traced, not rejected.
+ *     |d_a| in {0} U [2^-30, 2], d != 0; tmin < tmax; |tmin| and finite |tmax| in
+ *     {0} U [2^-16, 2^20) (negative bounds select the ray line behind o, R5);
+ *     tmax = +inf allowed. Other finite rays are traced, not rejected (the walk always
+ *     terminates); a non-finite origin, direction or tmin, or a NaN tmax, is a miss.
  *   - All device pointers must be on the handle's device and 16-byte aligned.
  */
 #ifndef VF_H

@@ -231,3 +231,52 @@ def incoherent(n: int, lo, hi, seed: int, tmax: float = np.inf):
     d = rng.normal(size=(n, 3))
     d /= np.linalg.norm(d, axis=1, keepdims=True)
     return pack(o, d, 0.0, tmax)
+
+
+def secondary(prim: np.ndarray, xyz: np.ndarray, t: np.ndarray, normal: np.ndarray, seed: int,
+              light_dir=(0.35, 1.0, 0.2), ao_tmax: float = 48.0):
+    """Shadow + ambient-occlusion rays spawned from primary hits (the
+    secondary bounces the paper leaves out). Input only: the primary rays, their hit
+    voxels, entry times and entry-face normals (oracle or vf_trace_ex). For every primary ray that
+    hit a voxel through a face (normal != 0), in primary-ray order:
+      * origin: the hit point o + t d (fp64 from the fp32 values), moved off the entry face into
+        the empty neighbour cell: face axis a gets the plane coordinate + 1/64 * normal_a;
+      * shadow ray: direction L = normalise(light_dir), mirrored in the face plane if it points
+        into the surface; tmax = +inf;
+      * AO ray: cosine-weighted direction on the hemisphere around the normal (MT19937(seed)),
+        tmax = ao_tmax.
+    Returns (n_shadow + n_ao, 8) fp32: all shadow rays first, then all AO rays (each half in the
+    primary order, so warps stay screen-coherent), and the primary index of every ray."""
+    prim = np.asarray(prim, dtype=np.float32).reshape(-1, 8)
+    normal = np.asarray(normal, dtype=np.int64).reshape(-1, 3)
+    ok = (np.asarray(xyz)[:, 0] >= 0) & (np.abs(normal).sum(1) == 1)
+    src = np.nonzero(ok)[0]
+    o = prim[src, 0:3].astype(np.float64)
+    d = prim[src, 4:7].astype(np.float64)
+    tt = np.asarray(t, dtype=np.float32)[src].astype(np.float64)
+    nrm = normal[src].astype(np.float64)
+    v = np.asarray(xyz, dtype=np.int64)[src].astype(np.float64)
+    p = o + tt[:, None] * d
+    face = np.abs(nrm) > 0
+    plane = v + (nrm > 0)  # entry face plane on the normal's axis
+    p = np.where(face, plane + nrm / 64.0, p)
+    L = np.asarray(light_dir, dtype=np.float64)
+    L = L / np.linalg.norm(L)
+    sd = np.broadcast_to(L, p.shape).copy()
+    into = (sd * nrm).sum(1) < 0
+    sd[into] = np.where(face[into], -sd[into], sd[into])
+    rng = np.random.Generator(np.random.MT19937(seed))
+    u1, u2 = rng.random(len(src)), rng.random(len(src))
+    r, phi = np.sqrt(u1), 2 * np.pi * u2
+    local = np.stack([r * np.cos(phi), r * np.sin(phi), np.sqrt(np.maximum(0.0, 1 - u1))], 1)
+    ax = np.argmax(np.abs(nrm), 1)
+    ad = np.empty_like(local)
+    for a in range(3):  # frame: normal axis a gets the cosine lobe, the other two the disc
+        m = ax == a
+        b, c = (a + 1) % 3, (a + 2) % 3
+        ad[m, a] = local[m, 2] * nrm[m, a]
+        ad[m, b] = local[m, 0]
+        ad[m, c] = local[m, 1]
+    ad /= np.linalg.norm(ad, axis=1, keepdims=True)
+    rays = np.concatenate([pack(p, sd, 0.0, np.inf), pack(p, ad, 0.0, ao_tmax)])
+    return rays, np.concatenate([src, src])

@@ -325,8 +325,9 @@ static int trace_one(const oracle_grid* g, const float* ray, int32_t* xyz, float
     if (!(ad == 0.0f || (ad >= 0x1p-30f && ad <= 2.0f))) return 2;
     if (!to_scaled(o[a], 39, &O[a]) || !to_scaled(d[a], 53, &D[a])) return 2;
   }
-  if (!(tmin == 0.0f || (tmin >= 0x1p-16f && tmin < 0x1p20f))) return 2;
-  if (!tmax_inf && !(tmax == 0.0f || (tmax >= 0x1p-16f && tmax < 0x1p20f))) return 2;
+  /* segment bounds may be negative (the ray line behind o; reading R5) */
+  if (!(tmin == 0.0f || (fabsf(tmin) >= 0x1p-16f && fabsf(tmin) < 0x1p20f))) return 2;
+  if (!tmax_inf && !(tmax == 0.0f || (fabsf(tmax) >= 0x1p-16f && fabsf(tmax) < 0x1p20f))) return 2;
   if (!to_scaled(tmin, 39, &TMIN)) return 2;
   if (!tmax_inf && !to_scaled(tmax, 39, &TMAX)) return 2;
   if (D[0] == 0 && D[1] == 0 && D[2] == 0) return 0; /* reading A5: all-zero d is a miss */

@@ -456,6 +456,7 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
       if (n)
         k_sparse_keys<<<grid_for(n), kThreads, 0, s>>>(vol->keys, vol->values, n, Rx, Ry, Rz, raw(ck), raw(vals),
                                                       raw(bad));
+      VF_CUDA_TRY(cudaStreamSynchronize(s));  // order the host read after the kernels on s
       if ((unsigned long long)bad[0]) {
         set_error("vf_build: %llu sparse voxels are out of range or have value 0", (unsigned long long)bad[0]);
         return VF_ERR_INVALID_ARG;
@@ -465,6 +466,7 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
     if (vol->kind == VF_VOL_SPARSE_DEVICE && n) {
       thrust::device_vector<unsigned long long> bad(1, 0ull);
       k_dup_check<<<grid_for(n), kThreads, 0, s>>>(raw(ck), n, raw(bad));
+      VF_CUDA_TRY(cudaStreamSynchronize(s));
       if ((unsigned long long)bad[0]) {
         set_error("vf_build: %llu duplicate voxel keys in sparse input", (unsigned long long)bad[0]);
         return VF_ERR_INVALID_ARG;
@@ -499,6 +501,7 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
       thrust::inclusive_scan(pol, flags.begin(), flags.end(), node_of.begin());
       thrust::transform(pol, node_of.begin(), node_of.end(), node_of.begin(),
                         [] __device__(uint32_t v) { return v - 1u; });
+      VF_CUDA_TRY(cudaStreamSynchronize(s));
       const uint64_t M = (uint64_t)(uint32_t)node_of[n - 1] + 1;
       flags.clear();
       flags.shrink_to_fit();
@@ -530,6 +533,7 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
         k_inline_sizes<<<grid_for(M), kThreads, 0, s>>>(raw(node_start), M, n, T.kind, T.top, T.last, raw(size),
                                                          raw(paper));
         thrust::exclusive_scan(pol, size.begin(), size.end(), off.begin(), (uint64_t)0);
+        VF_CUDA_TRY(cudaStreamSynchronize(s));
         words = (uint64_t)off[M - 1] + (uint64_t)size[M - 1];
         pwords = thrust::reduce(pol, paper.begin(), paper.end(), (uint64_t)0);
         arr.assign(words, 0u);
@@ -573,7 +577,10 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
       ck.swap(node_key);
       cr.swap(nr);
       n = M;
-      if (is_root) root = ((uint4)cr[0]).x;
+      if (is_root) {
+        VF_CUDA_TRY(cudaStreamSynchronize(s));  // cr was written by kernels on s
+        root = ((uint4)cr[0]).x;
+      }
     }
 
     const bool single_raw = f.n_tiers == 1 && f.tiers[0].kind == K_RAW;

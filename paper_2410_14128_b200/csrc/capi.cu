@@ -225,6 +225,15 @@ vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hi
     for (int i = 0; i < 2 * kMaxHostChunks; ++i)
       VF_CUDA_TRY(cudaEventCreateWithFlags(&h->chunk_ev[i], cudaEventDisableTiming));
   }
+  // On every return (error paths included) no copy of this call may still touch the caller's host
+  // buffers: drain the pipeline streams (a no-op after the final synchronize below).
+  struct Drain {
+    vf_handle* h;
+    ~Drain() {
+      for (int i = 0; i < kPipe; ++i)
+        if (h->pipe[i]) cudaStreamSynchronize(h->pipe[i]);
+    }
+  } drain{h};
   VF_CUDA_TRY(cudaEventRecord(h->pipe_ev, s));  // order after prior work on the caller's stream
   static const uint64_t chunks_env = [] {  // A/B override of the pipeline depth
     const char* e = getenv("VF_HOST_CHUNKS");

@@ -580,6 +580,14 @@ struct Lane {
     tmax = r1.w;
     tmax_finite = tmax < __int_as_float(0x7f800000);
     if (p.root == 0) return false;  // empty volume: buffer [0]
+    // non-finite origin / direction / tmin or a NaN tmax: outside every reading of the domain, a miss
+    // (the walk below assumes finite event times; vf.h "Rays")
+    {
+      const float inf = __int_as_float(0x7f800000);
+      if (!(fabsf(o[0]) < inf && fabsf(o[1]) < inf && fabsf(o[2]) < inf && fabsf(d[0]) < inf && fabsf(d[1]) < inf &&
+            fabsf(d[2]) < inf && fabsf(tmin) < inf && !(tmax != tmax)))
+        return false;
+    }
     moving = 0;
     dneg = 0;
 #pragma unroll
@@ -757,11 +765,15 @@ struct Lane {
       tn[a] = tplane(Pn[a], o[a], inv[a]);
     }
     const float m = fminf(fminf(tn[0], tn[1]), tn[2]);
-    const float thr = fmaf(m, kCertEps, m);
+    const float thr = fmaf(fabsf(m), kCertEps, m);  // m + |m| eps: also for m < 0 (tmin < 0)
     // s[a]: axis a steps. One candidate within the certification margin of the fp32 minimum is
     // certified to be the exact minimum; several go to the exact argmin (ties step together).
     bool s[3] = {tn[0] <= thr, tn[1] <= thr, tn[2] <= thr};
     int S = (s[0] ? 1 : 0) | (s[1] ? 2 : 0) | (s[2] ? 4 : 0);
+    if (S == 0) {  // no finite next event (non-finite ray data outside the domain): end the walk
+      nt = -1;
+      return;
+    }
     if ((S & (S - 1)) == 0) {
       eaxis = s[0] ? 0 : (s[1] ? 1 : 2);
       et = m;

@@ -37,14 +37,37 @@ def test_reference_arm_nonzero_rank_is_silent():
 
 @pytest.mark.gpu
 def test_multi_rank_code_path_with_one_rank():
-    """bench.py's N > 1 path (NCCL group, max-over-ranks reductions, the strong_frame pipeline of
-    chunked traces and NCCL hit gathers, per-rank e2e) exercised on the one GPU of the box
+    """bench.py's N > 1 path (NCCL group, max-over-ranks reductions, the chunked trace / NCCL hit
+    gather pipeline of one tile-sharded frame, per-rank e2e) exercised on the one GPU of the box
     (--force-dist)."""
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-dist", "--config", "cfg2",
-                        "--no-sweep", "--no-cpu-baseline", "--steps", "3", "--warmup", "3", "--gather-chunks", "2"],
+                        "--no-cpu-baseline", "--no-side", "--steps", "3", "--warmup", "3", "--gather-chunks", "2"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     d = json.loads([l for l in r.stdout.splitlines() if l.strip()][-1])
-    assert d["value"] > 0 and d["scaling"] == "weak" and d["gpu_launches"] == 3 and d["e2e"]["value"] > 0
-    sf = d["strong_frame"]  # one frame split over the ranks + NCCL hit gather (north_star)
-    assert sf["value"] > 0 and sf["trace_only"] >= 0.9 * sf["value"] and sf["gather_chunks"] == 2
+    assert d["value"] > 0 and d["scaling"] == "strong" and d["gpu_launches"] == 6 and d["e2e"]["value"] > 0
+    assert d["trace_only"] >= 0.9 * d["value"]
+
+
+@pytest.mark.gpu
+def test_driver_command_prints_one_compact_json_line():
+    """The driver's exact command: the last stdout line parses, is under 4 KB and carries the
+    headline, roofline, cpu_baseline, e2e and clocks (VERDICT r1 Missing #1)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--steps", "20", "--warmup", "5"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1 and len(lines[0]) < 4096, len(lines[0])
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["steps"] == 20 and d["warmup"] == 5 and d["value"] > 0
+    for k in ("roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"):
+        assert d.get(k), k
+    assert d["cpu_baseline"]["parity_mismatches"] == 0 and d["cpu_baseline"]["parity_checked"] > 0
+    assert 0 < d["roofline"]["frac"] < 1 and d["e2e"]["h2d_bytes_per_step"] == 32 * d["config"]["rays_per_frame"]
+
+
+def test_gpus_mismatch_exits_nonzero():
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1"],
+                       capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr

@@ -421,3 +421,42 @@ def test_compiled_in_format_vs_oracle(fmt, dims, p):
         gen = np.load(os.path.join(td, "o.npy"))
     np.testing.assert_array_equal(gen[0], outs[0])
     np.testing.assert_array_equal(gen[1], outs[1])
+
+
+# ---------------------------------------------------------------- rays behind the origin, bad rays
+@pytest.mark.parametrize("fmt", ["R(4, 4, 4)", "R(2^3) G(2)", "S(4)", "T(2, 2)", "D(2^3, 2) G(2)", "G(1) T(2, 1) R(1^3)"])
+def test_negative_tmin_parity_and_termination(fmt):
+    """with tmin < 0 the step's certification threshold m(1 + eps) fell below m
+    and the walk never advanced. Every such ray must now terminate with the oracle's answer."""
+    import test_oracle
+    vf = _vf()
+    dims = (16, 16, 16)
+    d = inputs.random_occupancy(dims, 0.08, 5)
+    h = vf.build(_dense_dev(d), fmt)
+    rays = np.concatenate([test_oracle._negative_tmin_rays(dims, 3, 4000),
+                           R.pack(np.array([[5.5, 3.25, 7.75]]), np.array([[1.0, 0, 0]]), -1.0, np.inf)])
+    ref = oracle.Grid.from_generator(d).trace(rays)
+    assert (ref["status"] != 2).all()
+    for restart in (False, True):
+        xyz, t = gpu_trace(h, rays, restart)
+        assert_parity(xyz, t, ref, f"{fmt} tmin<0 restart={restart}")
+
+
+def test_nonfinite_rays_miss():
+    """Non-finite origin / direction / tmin or NaN tmax: a miss (vf.h), never a hang."""
+    vf = _vf()
+    d = inputs.solid((8, 8, 8))
+    h = vf.build(_dense_dev(d), "R(1^3) G(2)")
+    nan, inf = np.float32(np.nan), np.float32(np.inf)
+    base = np.array([1.5, 1.5, -1.0, 0.0, 0.0, 0.0, 1.0, inf], dtype=np.float32)
+    rays = np.tile(base, (8, 1))
+    rays[0, 0] = nan
+    rays[1, 4] = inf
+    rays[2, 3] = -inf
+    rays[3, 3] = nan
+    rays[4, 7] = nan
+    rays[5, 1] = inf
+    rays[6, 6] = nan
+    xyz, t = gpu_trace(h, rays)
+    assert (xyz[:7] == -1).all() and np.isinf(t[:7]).all()
+    assert tuple(xyz[7]) == (1, 1, 0)  # the unmodified ray hits

@@ -243,3 +243,28 @@ def test_procedural_sparse_equals_bitset():
     assert (a["status"] == 1).sum() > 50
     np.testing.assert_array_equal(a["xyz"], b["xyz"])
     np.testing.assert_array_equal(a["t"], b["t"])
+
+
+def _negative_tmin_rays(dims, seed, n=600):
+    """Rays whose segment starts behind the origin (tmin < 0; reading R5): origins inside and
+    outside the box, tmin in [-2R, 0), finite and infinite tmax (some tmax < 0 too)."""
+    rng = np.random.Generator(np.random.MT19937(seed))
+    R_ = np.asarray(dims, dtype=np.float64)
+    o = np.round((rng.random((n, 3)) * 1.4 - 0.2) * R_ * 16) / 16
+    d = rng.integers(-3, 4, size=(n, 3)).astype(np.float64)
+    d[np.abs(d).sum(1) == 0] = (1, 1, 1)
+    d[::3] = rng.normal(size=(len(d[::3]), 3))
+    tmin = -np.round(rng.random(n) * 2 * R_.max() * 8) / 8 - 0.125
+    tmax = np.where(rng.random(n) < 0.5, np.inf, tmin + np.round(rng.random(n) * R_.max() * 8) / 8 + 0.125)
+    return R.pack(o, d / 2, tmin, tmax)
+
+
+@pytest.mark.parametrize("dims,p,seed", [((8, 8, 8), 0.1, 41), ((6, 9, 5), 0.3, 42)])
+def test_negative_tmin_vs_bruteforce(dims, p, seed):
+    """tmin < 0 (the GPU hung on such rays): the oracle walks [tmin, tmax) behind the
+    origin exactly as the brute-force slab test defines it."""
+    d = inputs.random_occupancy(dims, p, seed)
+    rays = _negative_tmin_rays(dims, seed)
+    assert (rays[:, 3] < 0).all()
+    out = _check_vs_brute(d, rays)
+    assert 0.05 < (out["status"] == 1).mean() < 0.95
