@@ -109,6 +109,9 @@ def lib():
         P = ctypes.POINTER(VgDesc)
         L.vg_dense_host.argtypes = [P, ctypes.c_void_p]
         L.vg_dense_host.restype = ctypes.c_int
+        L.vg_voxels_host.argtypes = [P, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+        L.vg_voxels_host.restype = ctypes.c_int
+        L.vg_sparse_objects.argtypes = [ctypes.c_uint32, ctypes.c_void_p]
         L.vg_voxel_host.argtypes = [P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
         L.vg_voxel_host.restype = ctypes.c_uint32
         L.vg_count_device.argtypes = [P, ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p]
@@ -133,6 +136,21 @@ def dense_host(d: VgDesc) -> np.ndarray:
 
 def voxel_host(d: VgDesc, x: int, y: int, z: int) -> int:
     return int(lib().vg_voxel_host(ctypes.byref(d), x, y, z))
+
+
+def voxels_host(d: VgDesc, xyz: np.ndarray) -> np.ndarray:
+    """Voxel words at the points xyz ((n, 3) int64; outside the volume -> 0)."""
+    p = np.ascontiguousarray(xyz, dtype=np.int64).reshape(-1, 3)
+    out = np.empty(len(p), dtype=np.uint32)
+    assert lib().vg_voxels_host(ctypes.byref(d), p.ctypes.data, len(p), out.ctypes.data) == 0
+    return out
+
+
+def sparse_objects(seed: int = 0x4096) -> np.ndarray:
+    """G5 object table (4096, 6) int32: cx, cy, cz, r, box, col."""
+    out = np.empty((4096, 6), dtype=np.int32)
+    lib().vg_sparse_objects(seed & 0xFFFFFFFF, out.ctypes.data)
+    return out
 
 
 def voxels_device(d: VgDesc, stream=None):

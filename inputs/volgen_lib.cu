@@ -273,6 +273,31 @@ int vg_dense_host(const vg_desc* d, uint32_t* out) {
   return 0;
 }
 
+// Voxel words at n points xyz (n x 3 int64) on the host (any generator; sparse through the
+// 64^3-bin object table, built once per call). Points outside the volume read 0.
+int vg_voxels_host(const vg_desc* d, const int64_t* xyz, uint64_t n, uint32_t* out) {
+  SparseTable t;
+  if (d->gen == VG_SPARSE) build_sparse_table(d, &t);
+  for (uint64_t i = 0; i < n; ++i) {
+    const int64_t x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    if (x < 0 || y < 0 || z < 0 || x >= d->dims[0] || y >= d->dims[1] || z >= d->dims[2]) {
+      out[i] = 0;
+      continue;
+    }
+    out[i] = d->gen == VG_SPARSE ? sparse_voxel(*d, t.nb, t.start.data(), t.objs.data(), x, y, z) : vg_voxel(d, x, y, z);
+  }
+  return 0;
+}
+
+// The G5 object table: out[6k..6k+5] = {cx, cy, cz, r, box, col} of object k (k < 4096).
+void vg_sparse_objects(uint32_t seed, int32_t* out) {
+  for (uint32_t k = 0; k < VG_SPARSE_OBJECTS; ++k) {
+    const vg_object o = vg_sparse_object(k, seed);
+    const int32_t v[6] = {o.c[0], o.c[1], o.c[2], o.r, o.box, (int32_t)o.col};
+    memcpy(out + 6 * k, v, sizeof(v));
+  }
+}
+
 // Single voxel on the host (any generator; sparse via brute force over objects).
 uint32_t vg_voxel_host(const vg_desc* d, int64_t x, int64_t y, int64_t z) {
   if (d->gen == VG_SPARSE) {

@@ -51,6 +51,8 @@ def lib():
         L.oracle_grid_slab_counts.argtypes = [vp, vp]
         L.oracle_grid_get.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
         L.oracle_grid_get.restype = ctypes.c_int
+        L.oracle_grid_get_many.argtypes = [vp, vp, ctypes.c_int64, vp]
+        L.oracle_grid_box.argtypes = [vp, vp, vp, vp]
         L.oracle_trace.argtypes = [vp, vp, ctypes.c_int64, vp, vp, vp, vp, vp, ctypes.c_int]
         L.oracle_trace.restype = ctypes.c_int64
         L.oracle_max_threads.restype = ctypes.c_int
@@ -93,6 +95,21 @@ class Grid:
 
     def get(self, x, y, z) -> int:
         return int(lib().oracle_grid_get(self._p, x, y, z))
+
+    def get_many(self, xyz: np.ndarray) -> np.ndarray:
+        """Occupancy (0/1 uint8) at the points xyz ((n, 3) int64, inside the volume)."""
+        p = np.ascontiguousarray(xyz, dtype=np.int64).reshape(-1, 3)
+        out = np.empty(len(p), dtype=np.uint8)
+        lib().oracle_grid_get_many(self._p, p.ctypes.data, len(p), out.ctypes.data)
+        return out
+
+    def box(self, lo, ext) -> np.ndarray:
+        """Occupancy of the box [lo, lo + ext) as a (ez, ey, ex) uint8 array."""
+        lo_ = np.asarray(lo, dtype=np.int64)
+        ex_ = np.asarray(ext, dtype=np.int64)
+        out = np.empty((int(ex_[2]), int(ex_[1]), int(ex_[0])), dtype=np.uint8)
+        lib().oracle_grid_box(self._p, lo_.ctypes.data, ex_.ctypes.data, out.ctypes.data)
+        return out
 
     def trace(self, rays: np.ndarray, nthreads: int = 0, with_steps: bool = False):
         """rays: (n, 8) float32 (vf_ray layout). Returns dict(xyz (n,3) int32, t (n,) float32,

@@ -35,7 +35,19 @@
  *   that attains it, stop at t_end, 6. t rounded to fp32 via long double.
  * Parallelism: OpenMP over rays, dynamic chunks of 256 (order-independent result).
  *
- * Rays outside the canonical domain are reported with status 2 (not traced).
+ * Rays outside the canonical domain are reported with status 2 (not traced). The segment bounds
+ * may be negative (|tmin|, finite |tmax| in {0} U [2^-16, 2^20): the ray line behind o, reading R5).
+ *
+ * PINS (tests/test_oracle.py; none of these functions is "parity unpinned"; mutation check in
+ * profiles/r2_oracle_mutations.md, 18 of 18 plausible mistakes turn a pin red):
+ *   trace_one / oracle_trace : exact brute force (tests/brute/brute.c, >= 1e5 rays per size 4^3..32^3,
+ *                              and tests/brute_force.py in Fractions), sphere / Menger / box closed forms,
+ *                              mirror symmetry, empty / solid volumes;
+ *   grid_from_generator      : per voxel vs the input library's evaluators (dense_host, voxels_host,
+ *                              the lowest-k brute force of volgen.h);
+ *   grid_procedural (G5 bins): every voxel of every object's AABB faces at 4096^3 and whole boxes;
+ *   grid_from_dense          : every voxel (incl. the last) vs the input array;
+ *   grid_slab_counts / count : per-slab sums of the input array.
  */
 #include <math.h>
 #include <omp.h>
@@ -226,6 +238,21 @@ void oracle_grid_slab_counts(const oracle_grid* g, uint64_t* out) {
 }
 
 int oracle_grid_get(const oracle_grid* g, int64_t x, int64_t y, int64_t z) { return occupied(g, x, y, z); }
+
+/* occupancy at n points (n x 3 int64, inside the volume), any grid mode */
+void oracle_grid_get_many(const oracle_grid* g, const int64_t* xyz, int64_t n, uint8_t* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) out[i] = (uint8_t)occupied(g, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
+}
+
+/* occupancy of the box [lo, lo + ext) as x-fastest bytes, any grid mode */
+void oracle_grid_box(const oracle_grid* g, const int64_t lo[3], const int64_t ext[3], uint8_t* out) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t z = 0; z < ext[2]; ++z)
+    for (int64_t y = 0; y < ext[1]; ++y)
+      for (int64_t x = 0; x < ext[0]; ++x)
+        out[x + ext[0] * (y + ext[1] * z)] = (uint8_t)occupied(g, lo[0] + x, lo[1] + y, lo[2] + z);
+}
 
 /* ------------------------------------------------------------------ exact times (step 2) */
 /* A time value: PLANE event T = N/D * 2^14 (D != 0), SCALAR T = tau * 2^-39, or +INF. */
