@@ -1,0 +1,105 @@
+"""Full-frame GPU parity at BASELINE.json's full sizes: EVERY ray of each
+config's frame, in the launch configuration bench.py times, against the oracle walking the dense
+occupancy bitset with OpenMP on the box's host cores.
+
+Bar (north_star; tests/parity.py): hit voxel and miss flag bit-exact, t within 1e-4 relative.
+"""
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+from parity import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@functools.lru_cache(maxsize=2)
+def _frame(cfg):
+    """(volume, rays, perm, oracle result over the whole frame) — one bitset per volume."""
+    import bench
+    vol = bench.make_volume(bench.CONFIGS[cfg][0])
+    rays, perm = bench.make_rays(cfg)
+    g = oracle.Grid.from_generator(vol)
+    ref = g.trace(rays)
+    g.close()
+    assert (ref["status"] != 2).all()
+    return vol, rays, perm, ref
+
+
+def _handles(vol, fmts):
+    import torch
+    from paper_2410_14128_b200 import vf
+    keys, rgba = inputs.voxels_device(vol)
+    for fmt in fmts:
+        h = vf.build((keys, rgba, inputs.dims_of(vol)), fmt)
+        yield fmt, h
+        h.close()
+    del keys, rgba
+    torch.cuda.empty_cache()
+
+
+def _check(cfg, fmts, incoherent=False):
+    import torch
+    vol, rays, _, ref = _frame(cfg)
+    rt = torch.from_numpy(rays).cuda()
+    hits = torch.empty((len(rays), 4), dtype=torch.int32, device="cuda")
+    for fmt, h in _handles(vol, fmts):
+        for restart in (False, True):
+            h.trace(rt, hits, restart=restart, incoherent=incoherent)  # as bench.py launches it
+            out = hits.cpu().numpy()
+            assert_parity(out[:, :3], out[:, 3].view(np.float32), ref, f"{cfg} {fmt} restart={restart} (full frame)")
+
+
+def test_cfg1_full_frame():
+    import bench
+    _check("cfg1", bench.SWEEP["cfg1"])
+
+
+def test_cfg2_full_frame():
+    import bench
+    _check("cfg2", bench.SWEEP["cfg2"])
+
+
+def test_cfg3_full_frame():
+    import bench
+    _check("cfg3", bench.SWEEP["cfg3"])
+
+
+def test_cfg4_full_frame():
+    import bench
+    _check("cfg4", list(dict.fromkeys(bench.SWEEP["cfg4"] + ["R(11, 11, 11)"])))
+
+
+def test_cfg4i_full_frame():
+    import bench
+    _check("cfg4i", bench.SWEEP["cfg4i"], incoherent=True)
+
+
+def test_cfg5_full_frame_every_sweep_format():
+    """cfg5 (4096^3, 3840x2160 = 8,294,400 rays): the bench's headline R(4^3) G(8) and every other
+    format of the cfg5 sweep, each over the whole frame, stack and restart."""
+    import bench
+    _check("cfg5", bench.SWEEP["cfg5"])
+
+
+def test_cfg5_tile_sharded_frame_assembled(tmp_path):
+    """The bench's multi-GPU frame path (interleaved 16x16 tiles, chunked trace + NCCL gather to
+    rank 0, shard.assemble) with every shard traced, assembled into the image and compared with
+    the oracle pixel by pixel. The pool exposes one GPU, so the ranks run one after another in a
+    one-rank NCCL group per shard world (bench.FrameStep with --force-dist semantics)."""
+    import os
+    import subprocess
+    import sys
+    vol, rays, perm, ref = _frame("cfg5")
+    np.save(tmp_path / "ref_xyz.npy", ref["xyz"])
+    np.save(tmp_path / "ref_t.npy", ref["t"])
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "frame_worker.py"), str(tmp_path)],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "FRAME OK" in r.stdout

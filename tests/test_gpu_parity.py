@@ -226,48 +226,6 @@ def test_trace_host_matches_device():
     np.testing.assert_array_equal(out[:, 3].view(np.float32), t)
 
 
-# ---------------------------------------------------------------- full-size configs (sampled)
-FULL = [
-    ("cfg3", "T(2, 2) T(2, 1) R(4, 4, 4)"), ("cfg3", "T(2, 1) T(2, 2) R(4, 4, 4)"), ("cfg3", "S(5) R(5, 5, 5)"),
-    ("cfg3", "G(10)"),
-    ("cfg4", "R(4, 4, 4) G(7)"), ("cfg4", "R(3, 3, 3) G(8)"), ("cfg4", "S(11)"), ("cfg4", "R(1, 1, 1) T(2, 5)"),
-    ("cfg4", "T(2, 4) R(3, 3, 3)"), ("cfg4", "R(11, 11, 11)"),
-    ("cfg5", "R(4, 4, 4) G(8)"), ("cfg5", "T(2, 6)"), ("cfg4i", "R(4, 4, 4) G(7)"), ("cfg4i", "S(11)"),
-]
-
-
-@pytest.mark.parametrize("cfg,fmt", FULL)
-def test_full_size_sampled(cfg, fmt):
-    """BASELINE.json full sizes, the bench's launch configuration, every 37th ray of the frame
-    (plus the street-level city camera) against the oracle walking the procedural occupancy."""
-    import torch
-    import bench
-    vf = _vf()
-    vname = bench.CONFIGS[cfg][0]
-    vol = bench.make_volume(vname)
-    keys, rgba = inputs.voxels_device(vol)
-    h = vf.build((keys, rgba, inputs.dims_of(vol)), fmt)
-    del keys, rgba
-    torch.cuda.empty_cache()
-    rays, _ = bench.make_rays(cfg)
-    idx = np.arange(0, len(rays), 37)
-    sample = [rays[idx]]
-    if cfg == "cfg4":
-        street, _ = R.camera("city_street", scale=8)
-        sample.append(street)
-    sample = np.concatenate(sample)
-    ref = oracle.Grid.procedural(vol).trace(sample)
-    rt = torch.from_numpy(rays).cuda()
-    for restart in (False, True):
-        out = h.trace(rt, restart=restart, incoherent=(cfg == "cfg4i")).cpu().numpy()  # as bench.py launches it
-        xyz, t = out[idx, :3], out[idx, 3].view(np.float32)
-        if cfg == "cfg4":
-            x2, t2 = gpu_trace(h, sample[len(idx):], restart)
-            xyz, t = np.concatenate([xyz, x2]), np.concatenate([t, t2])
-        assert_parity(xyz, t, ref, f"{cfg} {fmt} restart={restart}")
-    h.close()
-
-
 # ---------------------------------------------------------------- DF distance field
 @pytest.mark.parametrize("fmt,M", [("D(4, 4, 4, 5)", 5), ("R(1^3) D(3^3, 6)", 6), ("D(4, 3, 4, 2)", 2)])
 def test_df_distances_are_exact_l1(fmt, M):
@@ -325,7 +283,7 @@ def _table2():
 @pytest.mark.parametrize("res", [512, 2048])
 def test_table2_formats_parity(res):
     """Every format of PAPER.md Table 2 (rows 1-20 at 2048^3 on the cfg4 city, rows 21-40 at
-    512^3 on the t512 city), stack and restart, against the oracle on a strided frame sample."""
+    512^3 on the t512 city), stack and restart, against the oracle on every ray of the frame."""
     import torch
     import bench
     vf = _vf()
@@ -333,8 +291,8 @@ def test_table2_formats_parity(res):
     vol = bench.make_volume(bench.CONFIGS[cfg][0])
     keys, rgba = inputs.voxels_device(vol)
     rays, _ = bench.make_rays(cfg)
-    idx = np.arange(0, len(rays), 97)
-    ref = oracle.Grid.procedural(vol).trace(rays[idx])
+    idx = np.arange(len(rays))  # every ray of the frame
+    ref = oracle.Grid.from_generator(vol).trace(rays)
     rt = torch.from_numpy(rays).cuda()
     for label, r, sig in _table2():
         if r != res:

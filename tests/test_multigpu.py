@@ -172,3 +172,58 @@ def test_chunked_gather_over_nccl_single_rank():
     ok = q.get(timeout=300)
     p.join(60)
     assert p.exitcode == 0 and ok
+
+
+def _bench_frame_worker(rank, world, port, q):
+    """bench.py's N > 1 step on CPU/gloo: FrameStep (chunked trace of this rank's interleaved
+    tiles + async gather to rank 0) with a stand-in tracer, bench.max_over_ranks, assembly."""
+    import sys
+    import torch
+    import torch.distributed as dist
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    from paper_2410_14128_b200 import shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    width, height = 200, 120  # ragged last tile row/column
+    perm = R.tile_order(width, height)
+    own = shard.shard(perm, width, rank, world)
+    counts = shard.shard_counts(perm, width, world)
+    # "rays": the pixel index of each ray; the stand-in trace writes a record derived from it
+    rays = torch.from_numpy(perm[own].astype(np.int32))
+
+    def trace(rv, hv):
+        hv[:, 0] = rv
+        hv[:, 1] = rv * 3
+        hv[:, 2] = -rv
+        hv[:, 3] = rv % 7
+
+    step = bench.FrameStep(trace, rays, counts, rank, world, True, torch.device("cpu"), chunks=3, timed=False)
+    got = step()
+    mx = bench.max_over_ranks([float(rank + 1), 10.0 - rank], torch.device("cpu"), True)
+    if rank == 0:
+        img = shard.assemble(got, perm, width, world)
+        q.put((img, mx, step.launches))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_frame_step_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_frame_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    img, mx, launches = q.get(timeout=180)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    pix = np.arange(200 * 120)
+    np.testing.assert_array_equal(img[:, 0], pix)
+    np.testing.assert_array_equal(img[:, 1], pix * 3)
+    np.testing.assert_array_equal(img[:, 2], -pix)
+    np.testing.assert_array_equal(img[:, 3], pix % 7)
+    assert mx == [2.0, 10.0] and launches == 3
