@@ -474,7 +474,7 @@ def run_ours(args):
         except Exception:
             ent = {}
         achieved = launch_bytes / (kmean_ms / 1e3) / 1e9
-        ent_rays = ent.get("rays", n_total)  # ncu entries without a ray count were full-frame launches
+        ent_rays = ent.get("rays") or n_total  # ncu entries without a ray count were full-frame launches
         traffic = None
         if ent.get("dram_bytes_per_launch"):
             traffic = round(ent["dram_bytes_per_launch"] / ent_rays * rays.shape[0] / step.launches)

@@ -326,6 +326,8 @@ TraceParams make_trace_params(const Format& f, uint32_t root) {
   p.n_tiers = f.n_tiers;
   p.root = root;
   p.refill = 16;  // A/B on incoherent rays (cfg4i): 16 best of 8/16/24/32
+  p.chunk = 128;   // chunked trace (A/B)
+  p.crefill = 16;
   return p;
 }
 

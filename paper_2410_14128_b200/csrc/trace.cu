@@ -299,6 +299,7 @@ __device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, ui
 // (pure arithmetic in t; a packed compile-time table variant measured 2-8 % slower)
 struct NoSpec {
   static constexpr bool kStatic = false;
+  static constexpr uint32_t kTopWords = 0;  // words of a stageable top Raw grid (0: none)
 };
 
 // An optional cubic Raw top level R(A^3) (A = 0: none) over one sparse level of NS tiers of one
@@ -307,6 +308,7 @@ struct NoSpec {
 template <uint32_t A, uint32_t KIND, uint32_t LF, uint32_t NS, bool DFTOP = false>
 struct TopSparse {
   static constexpr bool kStatic = true;
+  static constexpr uint32_t kTopWords = (A > 0 && A <= 4 && !DFTOP) ? (1u << (3 * A)) : 0u;
   // DFTOP: the top level is a DF grid D(A^3, M) (2-word cells {TermInt, L1 distance})
   __device__ static __forceinline__ bool df(int t) { return DFTOP && A > 0 && t == 0; }
   static constexpr int OFF = A > 0 ? 1 : 0;
@@ -337,6 +339,7 @@ using RawSvdag = TopSparse<A, K_SVDAG, 1, M>;
 template <uint32_t NR, uint32_t A0, uint32_t A1, uint32_t A2, uint32_t DFM, uint32_t KIND, uint32_t NS>
 struct RawChain {
   static constexpr bool kStatic = true;
+  static constexpr uint32_t kTopWords = 0;
   static constexpr int NT = (int)(NR + NS);
   static constexpr uint32_t L2 = NS, L1 = NS + (NR > 2 ? A2 : 0u), L0 = L1 + (NR > 1 ? A1 : 0u);  // lc of raw tiers
   __host__ __device__ static constexpr uint32_t LCR(int t) { return t == 0 ? (NR == 1 ? NS : NR == 2 ? NS + A1 : L0) : t == 1 ? (NR == 2 ? NS : L1) : L2; }
@@ -371,6 +374,7 @@ struct RawChain {
 template <uint32_t A, uint32_t K1, uint32_t N1, uint32_t K2, uint32_t N2>
 struct TwoSparse {
   static constexpr bool kStatic = true;
+  static constexpr uint32_t kTopWords = 0;
   __device__ static __forceinline__ bool df(int) { return false; }
   static constexpr int OFF = A > 0 ? 1 : 0;
   static constexpr int B = OFF + (int)N1;  // first tier of the second sparse level
@@ -398,6 +402,7 @@ struct TwoSparse {
 template <uint32_t KIND, uint32_t LF, uint32_t NS, uint32_t A, uint32_t LASTM, uint32_t TOPM>
 struct SparseRaw {
   static constexpr bool kStatic = true;
+  static constexpr uint32_t kTopWords = 0;
   __device__ static __forceinline__ bool df(int) { return false; }
   static constexpr uint32_t LC0 = LF * (NS - 1) + A;  // lc of tier 0
   __device__ static __forceinline__ uint32_t lc(int t) { return t == (int)NS ? 0u : LC0 - LF * (uint32_t)t; }
@@ -441,9 +446,10 @@ enum { IT_CONTINUE = 0, IT_HIT = 1, IT_MISS = 2 };
 //
 // D (a format descriptor above) compiles the format in: with D::kStatic the tier geometry and
 // flags are functions of the tier index (no tier table, fewer live registers).
-template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec>
+template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec, bool STAGE = false>
 struct Lane {
   static constexpr bool SPEC = D::kStatic;
+  const uint32_t* s_top;  // STAGE: the top Raw grid (tier 0's node, D::kTopWords words) in shared memory
   float o[3], d[3], inv[3];  // inv = RN(1/d); +inf on axes with d = 0 (their next plane is never)
   float tmax;
   int V[3];       // finest voxel of the current cell (bits below lc(t) valid unless stale)
@@ -669,7 +675,8 @@ struct Lane {
         // 64-bit index: a single-level R(11^3) grid has 2^33 cells (reading A15)
         const size_t lin = (size_t)lx + ((size_t)ly << sx()) + ((size_t)lz << sxy());
         if (!is_df()) {
-          child = __ldg(buf + (size_t)N + lin);
+          if constexpr (STAGE) child = t == 0 ? s_top[lin] : __ldg(buf + (size_t)N + lin);
+          else child = __ldg(buf + (size_t)N + lin);
           occ = child != 0u;
           ct.add(VF_CTR_RAW_CELLS);
           ct.add(VF_CTR_FORMAT_BYTES, 4);
@@ -1004,6 +1011,96 @@ __global__ void __launch_bounds__(kPersistThreads, VF_PMINB) trace_persistent(co
   }
 }
 
+// Persistent warps over claimed chunks of p.chunk consecutive rays. The ray buffer is in screen-tile
+// order (16x16 blocks of 8x4 warp tiles), so a chunk is a screen-coherent patch: a warp claims a
+// chunk (one atomicAdd), starts its first 32 rays, and whenever >= p.crefill lanes are idle refills
+// them with the chunk's next rays — neighbours of the rays still in flight, so the warp stays
+// coherent while its finished lanes get work; when the chunk runs out the warp claims the next one.
+// Removes the launch tail (no waves: each warp keeps claiming until the frame is done) and most of
+// the in-warp tail of finished lanes. STAGE: the top Raw grid (<= 16 KB) is copied to shared memory
+// once per block and tier-0 cell tests read it there. work[0] = next ray, work[1] = finished blocks.
+template <uint32_t KINDS, bool RESTART, class D, bool STAGE>
+__global__ void __launch_bounds__(kTraceThreads, D::kStatic ? VF_MINB_SPEC : VF_MINB)
+    trace_chunked(const TraceParams p, const uint32_t* __restrict__ buf, const float4* __restrict__ rays,
+                  int4* __restrict__ hits, uint64_t n, unsigned long long* __restrict__ counters,
+                  unsigned long long* __restrict__ work) {
+  __shared__ __align__(16) uint32_t s_tw[8 * VF_MAX_TIERS];
+  extern __shared__ __align__(16) uint32_t s_top[];
+  if constexpr (STAGE) {
+    for (uint32_t i = threadIdx.x; i < D::kTopWords / 4; i += blockDim.x)
+      reinterpret_cast<uint4*>(s_top)[i] = __ldg(reinterpret_cast<const uint4*>(buf + p.root) + i);
+  }
+  stage_tiers(p, s_tw);  // (its __syncthreads also publishes s_top)
+  Ctr<false> ct;
+  Lane<KINDS, RESTART, false, D, STAGE> L;
+  L.s_top = s_top;
+  uint32_t stk[VF_MAX_TIERS];
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned lt = (1u << lane) - 1u;
+  bool active = false;
+  uint64_t idx = 0;
+  unsigned long long next = 0, end = 0;  // the warp's current chunk [next, end)
+  bool exhausted = false;
+  const unsigned keep = 32u - p.crefill;  // the inner loop runs while more than `keep` lanes trace
+  for (;;) {
+    // ---- refill (warp-uniform): claim a chunk when the current one is used up, start new rays
+    unsigned idle = __ballot_sync(0xffffffffu, !active);
+    if (next >= end && !exhausted) {
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(work, (unsigned long long)p.chunk);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (b >= n) {
+        exhausted = true;
+      } else {
+        next = b;
+        end = b + p.chunk < n ? b + p.chunk : n;
+      }
+    }
+    if (next < end) {
+      const unsigned long long mine = next + __popc(idle & lt);
+      next = next + __popc(idle) < end ? next + __popc(idle) : end;
+      if (!active && mine < end) {
+        idx = mine;
+        if (L.start(p, buf, s_tw, __ldg(rays + 2 * idx), __ldg(rays + 2 * idx + 1), ct)) {
+          active = true;
+        } else {
+          hits[idx] = miss_record();
+          if (p.payload) p.payload[idx] = make_uint2(0u, 0u);
+        }
+      }
+    }
+    if (__ballot_sync(0xffffffffu, active) == 0u) {
+      if (exhausted && next >= end) break;
+      continue;
+    }
+    // ---- trace: the plain per-ray loop; with refill (crefill < 32) a lane also leaves it when no
+    // more than `keep` lanes of the warp are still tracing (no per-iteration vote otherwise)
+    if (active) {
+      int res;
+      for (;;) {
+        res = L.iterate(p, buf, s_tw, stk, ct);
+        if (res != IT_CONTINUE) break;
+        if (keep > 0 && (unsigned)__popc(__activemask()) <= keep) break;
+      }
+      if (res != IT_CONTINUE) {
+        hits[idx] = res == IT_HIT ? L.hit_record() : miss_record();
+        if (p.payload) p.payload[idx] = res == IT_HIT ? L.payload_record(buf) : make_uint2(0u, 0u);
+        active = false;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long done = atomicAdd(work + 1, 1ull);
+    if (done == gridDim.x - 1) {  // last block: reset the work counter for the next launch
+      atomicExch(work, 0ull);
+      atomicExch(work + 1, 0ull);
+    }
+  }
+  (void)counters;
+}
+
 // ---- touch bitmap reduction (counting runs): distinct words = set bits; distinct 32-B sectors =
 // non-zero bytes (byte j of bitmap word i covers words 32i + 8j .. +7, one sector of the
 // 256-B-aligned buffer)
@@ -1112,8 +1209,17 @@ KernelFn select_kernel(uint32_t kinds, bool restart, bool count, bool persistent
 
 // Compiled-in formats: R(A^3) G(M) (RawSvdag: the cfg4 / cfg5 / t512 headline formats and their
 // sweep neighbours) and the cfg2 / cfg3 headline formats (SparseRaw). Others run the generic kernel.
+// mode 0: one thread per ray; 1: chunked persistent warps; 2: chunked + top Raw grid in shared memory
 template <uint32_t KINDS, class D>
-KernelFn spec_kernel(bool restart) {
+KernelFn spec_kernel(bool restart, int mode) {
+#ifdef VF_CHUNKED_KERNELS
+  if constexpr (D::kTopWords != 0) {
+    if (mode == 2) return restart ? trace_chunked<KINDS, true, D, true> : trace_chunked<KINDS, false, D, true>;
+  }
+  if (mode >= 1) return restart ? trace_chunked<KINDS, true, D, false> : trace_chunked<KINDS, false, D, false>;
+#else
+  (void)mode;
+#endif
   return restart ? trace_kernel<KINDS, true, false, D> : trace_kernel<KINDS, false, false, D>;
 }
 
@@ -1146,7 +1252,7 @@ bool same_format(const Format& f, const LevelSpec (&lv)[NL]) {
   return true;
 }
 
-KernelFn select_spec(const Format& f, bool restart) {
+KernelFn select_spec(const Format& f, bool restart, int mode) {
 #ifdef VF_ONLY_KINDS
   constexpr uint32_t K = VF_ONLY_KINDS;
 #define VF_HAS(k) (K == (k))
@@ -1157,7 +1263,7 @@ KernelFn select_spec(const Format& f, bool restart) {
     const uint8_t* e = f.levels[0].log2_extent;
     if (e[0] == e[1] && e[1] == e[2]) switch (((uint32_t)e[0] << 8) | f.levels[1].depth) {
 #define VF_SPEC(a, m) \
-  case ((a) << 8) | (m): return spec_kernel<5, RawSvdag<a, m>>(restart);
+  case ((a) << 8) | (m): return spec_kernel<5, RawSvdag<a, m>>(restart, mode);
         VF_SPEC(4, 7) VF_SPEC(4, 8) VF_SPEC(3, 8) VF_SPEC(3, 7) VF_SPEC(4, 5) VF_SPEC(2, 7) VF_SPEC(6, 5)
         VF_SPEC(8, 3) VF_SPEC(3, 5) VF_SPEC(3, 9) VF_SPEC(7, 2)
         VF_SPEC(2, 3) VF_SPEC(1, 4)  // small instances for the parity tests
@@ -1180,10 +1286,10 @@ KernelFn select_spec(const Format& f, bool restart) {
     const uint32_t key = (df << 28) | (a << 24) | (sp.kind << 16) | (lf << 8) | sp.depth;
     switch (key) {
 #define VF_TS(a, k, lf, ns, kinds) \
-  case ((a) << 24) | ((k) << 16) | ((lf) << 8) | (ns): return spec_kernel<kinds, TopSparse<a, K_OF_##k, lf, ns>>(restart);
+  case ((a) << 24) | ((k) << 16) | ((lf) << 8) | (ns): return spec_kernel<kinds, TopSparse<a, K_OF_##k, lf, ns>>(restart, mode);
 #define VF_DS(a, k, ns) /* DF top D(a^3, M) */ \
   case (1u << 28) | ((a) << 24) | ((k) << 16) | (1u << 8) | (ns): \
-    return spec_kernel<(1u << K_RAW) | (1u << K_OF_##k), TopSparse<a, K_OF_##k, 1, ns, true>>(restart);
+    return spec_kernel<(1u << K_RAW) | (1u << K_OF_##k), TopSparse<a, K_OF_##k, 1, ns, true>>(restart, mode);
       VF_DS(4, VF_SVDAG, 7) VF_DS(6, VF_SVDAG, 5) VF_DS(4, VF_SVO, 7) VF_DS(6, VF_SVO, 5) VF_DS(4, VF_SVDAG, 5)
       VF_DS(4, VF_SVO, 5) VF_DS(2, VF_SVDAG, 2)
 #undef VF_DS
@@ -1214,7 +1320,7 @@ KernelFn select_spec(const Format& f, bool restart) {
     if (ok) switch ((a << 24) | (l1.kind << 20) | ((uint32_t)l1.depth << 12) | (l2.kind << 8) | l2.depth) {
 #define VF_2S(a, k1, n1, k2, n2, kinds) \
   case ((a) << 24) | ((k1) << 20) | ((n1) << 12) | ((k2) << 8) | (n2): \
-    return spec_kernel<kinds, TwoSparse<a, K_OF_##k1, n1, K_OF_##k2, n2>>(restart);
+    return spec_kernel<kinds, TwoSparse<a, K_OF_##k1, n1, K_OF_##k2, n2>>(restart, mode);
         VF_2S(0, VF_SVO, 3, VF_SVDAG, 8, 6) VF_2S(0, VF_SVO, 5, VF_SVDAG, 6, 6) VF_2S(0, VF_SVO, 7, VF_SVDAG, 4, 6)
         VF_2S(4, VF_SVO, 3, VF_SVDAG, 4, 7)
         VF_2S(0, VF_SVO, 2, VF_SVDAG, 2, 6) VF_2S(1, VF_SVDAG, 1, VF_SVO, 2, 7)  // tests
@@ -1247,7 +1353,7 @@ KernelFn select_spec(const Format& f, bool restart) {
     if (ok && nr >= 1) switch ((nr << 28) | (a[0] << 24) | (a[1] << 20) | (a[2] << 16) | (dfm << 12) | (sk << 8) | ns) {
 #define VF_RC(nr, a0, a1, a2, dfm, k, ns, kinds) \
   case ((nr) << 28) | ((a0) << 24) | ((a1) << 20) | ((a2) << 16) | ((dfm) << 12) | ((k) << 8) | (ns): \
-    return spec_kernel<kinds, RawChain<nr, a0, a1, a2, dfm, K_OF_##k, ns>>(restart);
+    return spec_kernel<kinds, RawChain<nr, a0, a1, a2, dfm, K_OF_##k, ns>>(restart, mode);
       // single Raw / DF grids (cfg4 R(11^3), t512 R(9^3) / D(9^3, 6), cfg2 R(8^3), cfg1 R(6^3)); the
       // multi-level chains measured 1-13 % slower than the generic kernel and are not instantiated
       VF_RC(1, 11, 0, 0, 0, VF_NONE, 0, 1) VF_RC(1, 9, 0, 0, 0, VF_NONE, 0, 1) VF_RC(1, 9, 0, 0, 1, VF_NONE, 0, 1)
@@ -1257,39 +1363,46 @@ KernelFn select_spec(const Format& f, bool restart) {
       default: break;
     }
   }
-  if (same_format(f, kFmtG5R3)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 3, 0x10, 0x1>>(restart);
-  if (same_format(f, kFmtG2R2)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 2, 2, 0x2, 0x1>>(restart);
-  if (same_format(f, kFmtT22T21R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x6, 0x5>>(restart);
-  if (same_format(f, kFmtT21T22R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x5, 0x3>>(restart);
-  if (same_format(f, kFmtT11T12R1)) return spec_kernel<9, SparseRaw<K_NTREE, 1, 3, 1, 0x5, 0x3>>(restart);
-  if (same_format(f, kFmtS5R5)) return spec_kernel<3, SparseRaw<K_SVO, 1, 5, 5, 0x10, 0x1>>(restart);
-  if (same_format(f, kFmtT24R3)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 4, 3, 0x8, 0x1>>(restart);
-  if (same_format(f, kFmtT22T22R3)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 4, 3, 0xA, 0x5>>(restart);
-  if (same_format(f, kFmtT23R5)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 5, 0x4, 0x1>>(restart);
-  if (same_format(f, kFmtS5R4)) return spec_kernel<3, SparseRaw<K_SVO, 1, 5, 4, 0x10, 0x1>>(restart);
-  if (same_format(f, kFmtG5R4)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 4, 0x10, 0x1>>(restart);
+  if (same_format(f, kFmtG5R3)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 3, 0x10, 0x1>>(restart, mode);
+  if (same_format(f, kFmtG2R2)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 2, 2, 0x2, 0x1>>(restart, mode);
+  if (same_format(f, kFmtT22T21R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x6, 0x5>>(restart, mode);
+  if (same_format(f, kFmtT21T22R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x5, 0x3>>(restart, mode);
+  if (same_format(f, kFmtT11T12R1)) return spec_kernel<9, SparseRaw<K_NTREE, 1, 3, 1, 0x5, 0x3>>(restart, mode);
+  if (same_format(f, kFmtS5R5)) return spec_kernel<3, SparseRaw<K_SVO, 1, 5, 5, 0x10, 0x1>>(restart, mode);
+  if (same_format(f, kFmtT24R3)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 4, 3, 0x8, 0x1>>(restart, mode);
+  if (same_format(f, kFmtT22T22R3)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 4, 3, 0xA, 0x5>>(restart, mode);
+  if (same_format(f, kFmtT23R5)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 5, 0x4, 0x1>>(restart, mode);
+  if (same_format(f, kFmtS5R4)) return spec_kernel<3, SparseRaw<K_SVO, 1, 5, 4, 0x10, 0x1>>(restart, mode);
+  if (same_format(f, kFmtG5R4)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 4, 0x10, 0x1>>(restart, mode);
 #endif
 #undef VF_HAS
   return nullptr;
 }
 
 // resident blocks per SM for a persistent kernel (cached per function and device)
-int persistent_blocks(KernelFn fn, int device) {
+// bytes of the top Raw grid staged by the chunked kernels (mode 2): R(A^3) with A <= 4 on top
+size_t top_stage_bytes(const Format& f) {
+  const uint8_t* e = f.levels[0].log2_extent;
+  return f.levels[0].kind == VF_RAW ? (size_t)4 << (e[0] + e[1] + e[2]) : 0;
+}
+
+int persistent_blocks(KernelFn fn, int device, size_t smem = 0) {
   struct Entry {
     KernelFn fn;
     int dev, blocks;
+    size_t smem;
   };
   static Entry cache[256];
   static int n_cache = 0;
   static std::mutex mu;
   std::lock_guard<std::mutex> g(mu);
   for (int i = 0; i < n_cache; ++i)
-    if (cache[i].fn == fn && cache[i].dev == device) return cache[i].blocks;
+    if (cache[i].fn == fn && cache[i].dev == device && cache[i].smem == smem) return cache[i].blocks;
   int per_sm = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPersistThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPersistThreads, smem);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   int blocks = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
-  if (n_cache < 256) cache[n_cache++] = Entry{fn, device, blocks};
+  if (n_cache < 256) cache[n_cache++] = Entry{fn, device, blocks, smem};
   return blocks;
 }
 
@@ -1303,13 +1416,44 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
   const bool persistent = (flags & (VF_TRACE_PERSISTENT_WARPS | VF_TRACE_INCOHERENT)) != 0;
   KernelFn fn = select_kernel(kinds, (flags & VF_TRACE_RESTART_SV) != 0, counters != nullptr, persistent);
   static const bool no_spec = getenv("VF_NO_SPEC") != nullptr;  // A/B and tests: generic kernel only
+  static const int chunked_env = [] {  // A/B: force the chunked kernels (1) / with staged top grid (2)
+    const char* e = getenv("VF_CHUNKED");
+    return e ? atoi(e) : -1;
+  }();
+  int mode = (flags & VF_TRACE_CHUNKED) ? ((flags & VF_TRACE_STAGE_TOP) ? 2 : 1) : 0;
+  if (chunked_env >= 0) mode = chunked_env;
+  bool chunked = false;
   if (!persistent && !counters && !no_spec)
-    if (KernelFn sf = select_spec(h->fmt, (flags & VF_TRACE_RESTART_SV) != 0)) fn = sf;
+    if (KernelFn sf = select_spec(h->fmt, (flags & VF_TRACE_RESTART_SV) != 0, mode)) {
+      fn = sf;
+      chunked = mode > 0;
+    }
   if (!fn) {
     set_error("vf_trace: no kernel instantiated for kind set 0x%x", kinds);
     return VF_ERR_UNSUPPORTED;
   }
-  if (persistent) {
+  if (chunked) {
+    static const uint32_t chunk_env = [] {
+      const char* e = getenv("VF_CHUNK");
+      const int v = e ? atoi(e) : 0;
+      return (uint32_t)((v >= 32 && v % 32 == 0) ? v : 0);
+    }();
+    static const uint32_t crefill_env = [] {
+      const char* e = getenv("VF_CREFILL");
+      const int v = e ? atoi(e) : 0;
+      return (uint32_t)((v >= 1 && v <= 32) ? v : 0);
+    }();
+    TraceParams tp = h->tp;
+    tp.payload = reinterpret_cast<uint2*>(payload);
+    tp.touch = touch;
+    if (chunk_env) tp.chunk = chunk_env;
+    if (crefill_env) tp.crefill = crefill_env;
+    const uint32_t slot = h->work_slot.fetch_add(1) % kWorkSlots;
+    const size_t smem = mode == 2 ? top_stage_bytes(h->fmt) : 0;
+    const int blocks = persistent_blocks(fn, h->device, smem);
+    fn<<<blocks, kTraceThreads, smem, s>>>(tp, h->buf, reinterpret_cast<const float4*>(rays),
+                                           reinterpret_cast<int4*>(hits), n, counters, h->work + 2 * slot);
+  } else if (persistent) {
     static const int refill_env = [] {
       const char* e = getenv("VF_REFILL");
       const int v = e ? atoi(e) : 0;

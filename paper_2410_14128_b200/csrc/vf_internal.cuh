@@ -55,6 +55,8 @@ struct TraceParams {
   uint32_t top_mask;    // bit t: tier t is its level's top
   uint32_t last_mask;   // bit t: tier t is its level's last tier
   uint32_t refill;      // persistent trace: refill a warp when >= refill lanes are idle
+  uint32_t chunk;       // chunked trace: rays per claimed chunk (multiple of 32)
+  uint32_t crefill;     // chunked trace: refill from the warp's chunk when >= crefill lanes are idle
   uint32_t df_mask;     // bit t: tier t is a DF grid (2-word cells {TermInt, L1 distance})
   uint2* payload;       // optional closest-hit payload output (vf_trace_ex), per launch
   uint32_t* touch;      // counting launches: touch bitmap, one bit per format word (else null)
@@ -108,6 +110,10 @@ constexpr int kPipe = 4;
 constexpr int kMaxHostChunks = 64;
 // internal trace flag (ablation / tests): persistent warps with dynamic ray refill
 constexpr uint32_t VF_TRACE_PERSISTENT_WARPS = 1u << 30;
+// internal trace flags (A/B): persistent warps over claimed screen-coherent chunks (in-warp refill
+// from the chunk), optionally with the top Raw grid staged in shared memory
+constexpr uint32_t VF_TRACE_CHUNKED = 1u << 29;
+constexpr uint32_t VF_TRACE_STAGE_TOP = 1u << 28;
 
 // errors
 void set_error(const char* fmt, ...);

@@ -16,11 +16,11 @@ vol = bench.make_volume(bench.CONFIGS[cfg][0])
 k, c = inputs.voxels_device(vol)
 rays = torch.from_numpy(bench.make_rays(cfg)[0]).cuda()
 hits = torch.empty((rays.shape[0], 4), dtype=torch.int32, device="cuda")
-incoh = bench.CONFIGS[cfg][1] == "incoherent"
+incoh = bench.CONFIGS[cfg][1] in ("incoherent", "secondary")
 for fmt in bench.SWEEP[cfg]:
     h = vf.build((k, c, inputs.dims_of(vol)), fmt)
     for restart in (False, True):
         h.trace(rays, hits, restart=restart, incoherent=incoh)
         torch.cuda.synchronize()
-        print(f"LAUNCH {cfg}|{h.signature}|{'restart' if restart else 'stack'}", flush=True)
+        print(f"LAUNCH {cfg}|{h.signature}|{'restart' if restart else 'stack'} {rays.shape[0]}", flush=True)
     h.close()

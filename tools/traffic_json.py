@@ -21,16 +21,19 @@ for r in rows[hi + 1:]:
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6,
              "inst": 1, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9}.get(unit, 1)
     launch.setdefault(int(d["ID"]), {})[d["Metric Name"]] = v * scale
-keys = [l.split(" ", 1)[1].strip() for l in open(sys.argv[2]) if l.startswith("LAUNCH ")]
+launches = [l.split()[1:] for l in open(sys.argv[2]) if l.startswith("LAUNCH ")]
+keys = [" ".join(x[:-1]) if x[-1].isdigit() else " ".join(x) for x in launches]
+nrays = [int(x[-1]) if x[-1].isdigit() else None for x in launches]
 ids = sorted(launch)
 path = os.path.join(ROOT, "profiles", "traffic.json")
 tj = json.load(open(path)) if os.path.exists(path) else {}
-for key, i in zip(keys, ids):
+for key, i, nr in zip(keys, ids, nrays):
     m = launch[i]
     tj[key] = {"dram_bytes_per_launch": int(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)),
                "ncu_duration_ns": int(m.get("gpu__time_duration.sum", 0)),
                "warp_inst_per_launch": int(m.get("smsp__inst_executed.sum", 0)),
                "thread_inst_per_launch": int(m.get("smsp__thread_inst_executed.sum", 0)),
+               "rays": nr,
                "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
                          "smsp__inst_executed.sum,smsp__thread_inst_executed.sum "
                          "--clock-control none over tools/sweep_trace.py (cold cache, serialised)"}
