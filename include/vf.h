@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define VF_ABI_VERSION 1
+#define VF_ABI_VERSION 2 /* 2: vf_build takes a vf_allocator */
 
 #if defined(__GNUC__)
 #define VF_API __attribute__((visibility("default")))
@@ -116,11 +116,27 @@ typedef struct {
 /* ---------------------------------------------------------------- build */
 typedef struct vf_handle vf_handle; /* opaque; owns the format buffer; immutable after build */
 
+/* Device memory provider ("PyTorch only for device memory and streams"; the
+ * Python binding passes torch's caching allocator). Every device allocation of vf_build (the
+ * format buffer and all build temporaries) and of the handle's later calls (work counters,
+ * vf_trace_counters / vf_trace_host scratch) is requested through it:
+ *   alloc(bytes, ctx, stream) -> device pointer (16-B aligned) on the handle's device, or NULL;
+ *   free(ptr, bytes, ctx, stream) returns a block (bytes = the size requested), on the stream it
+ *   was requested for, after the library has synchronised every use of it.
+ * The struct is copied by vf_build; ctx and both functions must stay valid until vf_destroy.
+ * NULL allocator: cudaMalloc / cudaFree. */
+typedef struct {
+  void* (*alloc)(size_t bytes, void* ctx, void* cuda_stream);
+  void (*free)(void* ptr, size_t bytes, void* ctx, void* cuda_stream);
+  void* ctx;
+} vf_allocator;
+
 enum {
   VF_BUILD_WHOLE_LEVEL_DEDUP = 1u << 0, /* one SVDAG de-dup map per level across sub-volumes
                                            (§4.3; evaluated ON).
                                            Clear it for per-sub-volume maps (ablation). */
-  VF_BUILD_DEFAULT = VF_BUILD_WHOLE_LEVEL_DEDUP
+  VF_BUILD_DEFAULT = VF_BUILD_WHOLE_LEVEL_DEDUP,
+  VF_BUILD_KNOWN_FLAGS = VF_BUILD_WHOLE_LEVEL_DEDUP /* any other bit: VF_ERR_INVALID_ARG */
 };
 
 /* Build the format buffer on `device` (stream-ordered on cuda_stream, synchronous before
@@ -130,9 +146,14 @@ enum {
  * paddings are added (reported in vf_stats.paper_layout_bytes vs bytes_used): SVO children
  * blocks start at even words (8-B node loads), N^3-tree nodes at multiples of 4 words (16-B).
  * *bytes_used = 4 x device words including word 0. Level 1's resolution must equal dims.
- * On error *out is NULL and nothing is leaked. */
+ * alloc: device memory provider (above); NULL = cudaMalloc.
+ * Errors: VF_ERR_OVERFLOW when a tier would place a node at or beyond word 2^32 (its offset could
+ * not be stored, reading A15) — checked before that tier is allocated, so an
+ * oversized plan fails fast; a single Raw level stores no offsets and is exempt.
+ * VF_ERR_OOM when the allocator fails. On error *out is NULL and nothing is leaked. */
 VF_API vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_levels, uint32_t build_flags,
-                   int device, void* cuda_stream, vf_handle** out, uint64_t* bytes_used);
+                          const vf_allocator* alloc, int device, void* cuda_stream, vf_handle** out,
+                          uint64_t* bytes_used);
 
 /* ---------------------------------------------------------------- trace (the hot path) */
 typedef struct {

@@ -19,6 +19,7 @@
 // SVDAG de-duplication is exact hash-consing: records are sorted by a 64-bit content hash
 // and every record is compared word by word with its run leader (collisions fall back to a
 // scan of the run), so the stored node SET — and hence bytes_used — is deterministic.
+#include <thrust/device_malloc_allocator.h>
 #include <thrust/device_vector.h>
 #include <thrust/execution_policy.h>
 #include <thrust/iterator/counting_iterator.h>
@@ -33,6 +34,8 @@
 #include <thrust/functional.h>
 
 #include <chrono>
+#include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "vf_internal.cuh"
@@ -63,8 +66,51 @@ __host__ __device__ inline uint64_t morton(uint32_t x, uint32_t y, uint32_t z) {
   return spread3(x) | (spread3(y) << 1) | (spread3(z) << 2);
 }
 
+// ---------------------------------------------------------------- build memory
+// Every device allocation of a build — vectors and the algorithms' temporary storage — goes
+// through the caller's vf_allocator (vf_build's `alloc`; torch's caching allocator from Python),
+// requested on the build stream. The allocator of the running build is thread-local.
+thread_local const DevAllocator* tl_alloc = nullptr;
+thread_local cudaStream_t tl_stream = nullptr;
+
+void* build_get(size_t bytes) {
+  void* p = tl_alloc ? tl_alloc->get(bytes, tl_stream) : nullptr;
+  if (!p) throw std::bad_alloc();
+  return p;
+}
+void build_put(void* p, size_t bytes) {
+  if (tl_alloc) tl_alloc->put(p, bytes, tl_stream);
+}
+
 template <class T>
-T* raw(thrust::device_vector<T>& v) {
+struct BuildAlloc : thrust::device_malloc_allocator<T> {
+  using base = thrust::device_malloc_allocator<T>;
+  using pointer = typename base::pointer;
+  using size_type = typename base::size_type;
+  template <class U>
+  struct rebind {
+    typedef BuildAlloc<U> other;
+  };
+  BuildAlloc() = default;
+  template <class U>
+  BuildAlloc(const BuildAlloc<U>&) {}
+  pointer allocate(size_type n) { return pointer(static_cast<T*>(build_get(n * sizeof(T)))); }
+  void deallocate(pointer p, size_type n) noexcept { build_put(thrust::raw_pointer_cast(p), n * sizeof(T)); }
+};
+template <class T>
+using dvec = thrust::device_vector<T, BuildAlloc<T>>;
+
+struct TmpAlloc {  // temporary storage of thrust algorithms
+  typedef char value_type;
+  char* allocate(std::ptrdiff_t n) { return static_cast<char*>(build_get((size_t)n)); }
+  void deallocate(char* p, size_t n) { build_put(p, n); }
+};
+TmpAlloc g_tmp_alloc;
+
+inline auto policy(cudaStream_t s) { return thrust::cuda::par(g_tmp_alloc).on(s); }
+
+template <class V>
+auto raw(V& v) {
   return thrust::raw_pointer_cast(v.data());
 }
 
@@ -293,9 +339,9 @@ __global__ void k_inline_write(const uint64_t* ck, const uint4* cr, const uint64
 
 // ---------------------------------------------------------------- SVDAG tiers (de-duplicated)
 struct Records {  // m records of up to 9 words
-  thrust::device_vector<uint32_t> words;  // m * 9
-  thrust::device_vector<uint8_t> len;
-  thrust::device_vector<uint64_t> svid;
+  dvec<uint32_t> words;  // m * 9
+  dvec<uint8_t> len;
+  dvec<uint64_t> svid;
 };
 
 __device__ inline uint64_t mix64(uint64_t h) {
@@ -362,23 +408,27 @@ __global__ void k_rec_write(const uint32_t* words, const uint8_t* len, const uin
 // Hash-cons m records. Unique records are laid out in record order (first occurrence, i.e.
 // Morton order of the sub-volume that first needs them) starting at arr_off within `arr`
 // (whose global word offset is base). Returns words written; ptr[i] = global pointer.
-uint64_t dedup(Records& R, uint64_t m, thrust::device_vector<uint32_t>& arr, uint64_t arr_off, uint64_t base,
-               thrust::device_vector<uint32_t>& ptr, uint64_t* n_unique, cudaStream_t s) {
-  auto pol = thrust::cuda::par.on(s);
-  thrust::device_vector<uint64_t> h(m);
-  thrust::device_vector<uint32_t> sidx(m);
+uint64_t dedup(Records& R, uint64_t m, dvec<uint32_t>& arr, uint64_t arr_off, uint64_t base,
+               dvec<uint32_t>& ptr, uint64_t* n_unique, cudaStream_t s) {
+  auto pol = policy(s);
+  dvec<uint64_t> h(m);
+  dvec<uint32_t> sidx(m);
   k_rec_hash<<<grid_for(m), kThreads, 0, s>>>(raw(R.words), raw(R.len), raw(R.svid), m, raw(h), raw(sidx));
   thrust::sort_by_key(pol, h.begin(), h.end(), sidx.begin());  // radix sort: stable
-  thrust::device_vector<uint64_t> rs(m);
+  dvec<uint64_t> rs(m);
   k_run_flags<<<grid_for(m), kThreads, 0, s>>>(raw(h), m, raw(rs));
   thrust::inclusive_scan(pol, rs.begin(), rs.end(), rs.begin(), thrust::maximum<uint64_t>());
-  thrust::device_vector<uint32_t> rep(m), uw(m);
+  dvec<uint32_t> rep(m), uw(m);
   k_rep<<<grid_for(m), kThreads, 0, s>>>(raw(R.words), raw(R.len), raw(R.svid), raw(sidx), raw(rs), m, raw(rep),
                                           raw(uw));
-  thrust::device_vector<uint64_t> off(m);
+  dvec<uint64_t> off(m);
   thrust::transform_exclusive_scan(
       pol, uw.begin(), uw.end(), off.begin(), [] __device__(uint32_t v) { return (uint64_t)v; }, (uint64_t)arr_off,
       thrust::plus<uint64_t>());
+  {  // the host reads below follow the kernels on s
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("dedup: ") + cudaGetErrorString(e));
+  }
   uint64_t last_off = off[m - 1];
   uint32_t last_w = uw[m - 1];
   uint64_t total = last_off + last_w - arr_off;
@@ -427,20 +477,24 @@ __global__ void k_ptr_refs(const uint32_t* ptr, uint64_t M, uint4* nr) {
 // ---------------------------------------------------------------- driver
 vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cudaStream_t s, Handle* h) {
   auto t_start = std::chrono::steady_clock::now();
-  auto pol = thrust::cuda::par.on(s);
+  struct Scope {  // the allocator of this build, for every vector and algorithm below
+    Scope(const DevAllocator* a, cudaStream_t s) { tl_alloc = a, tl_stream = s; }
+    ~Scope() { tl_alloc = nullptr, tl_stream = nullptr; }
+  } scope(&h->alloc, s);
+  auto pol = policy(s);
   const bool whole = (flags & VF_BUILD_WHOLE_LEVEL_DEDUP) != 0;
   const uint32_t Rx = f.dims[0], Ry = f.dims[1], Rz = f.dims[2];
 
   try {
     // ---- step 0: non-empty voxels as (Morton key, rgba), sorted by key
-    thrust::device_vector<uint64_t> ck;
-    thrust::device_vector<uint32_t> vals;
+    dvec<uint64_t> ck;
+    dvec<uint32_t> vals;
     uint64_t n = 0;
     if (vol->kind == VF_VOL_DENSE_DEVICE) {
       const uint64_t total = (uint64_t)Rx * Ry * Rz;
       const uint32_t* rgba = vol->rgba;
       n = (uint64_t)thrust::count_if(pol, rgba, rgba + total, [] __device__(uint32_t v) { return v != 0u; });
-      thrust::device_vector<uint64_t> idx(n);
+      dvec<uint64_t> idx(n);
       if (n)
         thrust::copy_if(pol, thrust::counting_iterator<uint64_t>(0), thrust::counting_iterator<uint64_t>(total),
                         idx.begin(), [rgba] __device__(uint64_t i) { return rgba[i] != 0u; });
@@ -452,7 +506,7 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
       n = vol->n_voxels;
       ck.resize(n);
       vals.resize(n);
-      thrust::device_vector<unsigned long long> bad(1, 0ull);
+      dvec<unsigned long long> bad(1, 0ull);
       if (n)
         k_sparse_keys<<<grid_for(n), kThreads, 0, s>>>(vol->keys, vol->values, n, Rx, Ry, Rz, raw(ck), raw(vals),
                                                       raw(bad));
@@ -464,7 +518,7 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
     }
     if (n) thrust::sort_by_key(pol, ck.begin(), ck.end(), vals.begin());
     if (vol->kind == VF_VOL_SPARSE_DEVICE && n) {
-      thrust::device_vector<unsigned long long> bad(1, 0ull);
+      dvec<unsigned long long> bad(1, 0ull);
       k_dup_check<<<grid_for(n), kThreads, 0, s>>>(raw(ck), n, raw(bad));
       VF_CUDA_TRY(cudaStreamSynchronize(s));
       if ((unsigned long long)bad[0]) {
@@ -475,17 +529,29 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
     h->stats.nonempty_voxels = n;
 
     // ---- tiers, finest first
-    thrust::device_vector<uint4> cr(n);
+    dvec<uint4> cr(n);
     if (n) k_vals_to_refs<<<grid_for(n), kThreads, 0, s>>>(raw(vals), n, raw(cr));
     vals.clear();
     vals.shrink_to_fit();
 
-    std::vector<thrust::device_vector<uint32_t>> tier_words(f.n_tiers);
+    std::vector<dvec<uint32_t>> tier_words(f.n_tiers);
     std::vector<uint64_t> tier_base(f.n_tiers, 0);
     uint64_t cursor = 1;  // word 0 = root pointer
     uint64_t paper_words = 1;
     uint32_t root = 0;
 
+    // Stored offsets are u32 word addresses (16 GiB limit; reading A15): every node of
+    // a tier below the root is referenced by one, so it must end below 2^32 words; the root tier is
+    // referenced only by word 0 (its base). A single Raw level stores no offsets (64-bit indexing).
+    // Checked before a tier's words are allocated, so an oversized plan fails fast.
+    const bool single_raw = f.n_tiers == 1 && f.tiers[0].kind == K_RAW;
+    auto offsets_fit = [&](int t, uint64_t base, uint64_t words) {
+      if (single_raw) return true;
+      if (t == 0 ? base < (1ull << 32) : base + words <= (1ull << 32)) return true;
+      set_error("vf_build: tier %d needs words [%llu, %llu); stored offsets must stay below 2^32 words "
+                "(16 GiB, PAPER.md:86)", t, (unsigned long long)base, (unsigned long long)(base + words));
+      return false;
+    };
     for (int t = (int)f.n_tiers - 1; t >= 0 && n > 0; --t) {
       const Tier& T = f.tiers[t];
       const bool is_root = t == 0;
@@ -496,7 +562,7 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
       const uint64_t base = cursor;
       tier_base[t] = base;
 
-      thrust::device_vector<uint32_t> flags(n), node_of(n);
+      dvec<uint32_t> flags(n), node_of(n);
       k_flags<<<grid_for(n), kThreads, 0, s>>>(raw(ck), n, shift, raw(flags));
       thrust::inclusive_scan(pol, flags.begin(), flags.end(), node_of.begin());
       thrust::transform(pol, node_of.begin(), node_of.end(), node_of.begin(),
@@ -505,16 +571,17 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
       const uint64_t M = (uint64_t)(uint32_t)node_of[n - 1] + 1;
       flags.clear();
       flags.shrink_to_fit();
-      thrust::device_vector<uint64_t> node_start(M), node_key(M);
+      dvec<uint64_t> node_start(M), node_key(M);
       k_node_starts<<<grid_for(n), kThreads, 0, s>>>(raw(ck), raw(node_of), n, shift, raw(node_start), raw(node_key));
-      thrust::device_vector<uint4> nr(M);
-      thrust::device_vector<uint32_t>& arr = tier_words[t];
+      dvec<uint4> nr(M);
+      dvec<uint32_t>& arr = tier_words[t];
       uint64_t words = 0, pwords = 0, nodes = M;
 
       if (T.kind == K_RAW) {
         const uint64_t F = 1ull << (T.lf[0] + T.lf[1] + T.lf[2]);
         const uint32_t cw = T.df ? 2u : 1u;
         words = pwords = M * F * cw;
+        if (!offsets_fit(t, base, words)) return VF_ERR_OVERFLOW;
         arr.assign(words, 0u);
         k_raw_scatter<<<grid_for(n), kThreads, 0, s>>>(raw(ck), raw(cr), raw(node_of), n, is_root, lf, T.lf[0],
                                                         T.lf[1], F, cw, raw(arr));
@@ -529,18 +596,19 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
         }
         k_raw_refs<<<grid_for(M), kThreads, 0, s>>>(M, base, F * cw, raw(nr));
       } else if (T.kind == K_SVO || T.kind == K_NTREE) {
-        thrust::device_vector<uint64_t> size(M), paper(M), off(M);
+        dvec<uint64_t> size(M), paper(M), off(M);
         k_inline_sizes<<<grid_for(M), kThreads, 0, s>>>(raw(node_start), M, n, T.kind, T.top, T.last, raw(size),
                                                          raw(paper));
         thrust::exclusive_scan(pol, size.begin(), size.end(), off.begin(), (uint64_t)0);
         VF_CUDA_TRY(cudaStreamSynchronize(s));
         words = (uint64_t)off[M - 1] + (uint64_t)size[M - 1];
+        if (!offsets_fit(t, base, words)) return VF_ERR_OVERFLOW;
         pwords = thrust::reduce(pol, paper.begin(), paper.end(), (uint64_t)0);
         arr.assign(words, 0u);
         k_inline_write<<<grid_for(M), kThreads, 0, s>>>(raw(ck), raw(cr), raw(node_start), M, n, T.kind, is_root, T.top,
                                                          T.last, lf, raw(off), base, raw(arr), raw(nr));
       } else {  // K_SVDAG
-        thrust::device_vector<uint32_t> leafptr;
+        dvec<uint32_t> leafptr;
         uint64_t off = 0;
         if (T.last) {
           Records L;
@@ -560,11 +628,12 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
         k_node_records<<<grid_for(M), kThreads, 0, s>>>(raw(ck), raw(cr), T.last ? raw(leafptr) : nullptr,
                                                         raw(node_start), raw(node_key), M, n, is_root, T.last, whole,
                                                         T.depth, raw(Nn.words), raw(Nn.len), raw(Nn.svid));
-        thrust::device_vector<uint32_t> ptr;
+        dvec<uint32_t> ptr;
         uint64_t nu = 0;
         uint64_t w2 = dedup(Nn, M, arr, off, base, ptr, &nu, s);
         nodes = nu;
         words = pwords = off + w2;
+        if (!offsets_fit(t, base, words)) return VF_ERR_OVERFLOW;
         k_ptr_refs<<<grid_for(M), kThreads, 0, s>>>(raw(ptr), M, raw(nr));
       }
       if (t < VF_MAX_TIERS) {
@@ -583,22 +652,17 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
       }
     }
 
-    const bool single_raw = f.n_tiers == 1 && f.tiers[0].kind == K_RAW;
-    if (!single_raw && cursor >= (1ull << 32)) {
-      set_error("vf_build: buffer needs %llu words; stored offsets must stay below 2^32 words (16 GiB, PAPER.md:86)",
-                (unsigned long long)cursor);
-      return VF_ERR_OVERFLOW;
-    }
     // ---- assemble: word 0 = root pointer, then each tier at its base
     // 8 zero guard words after the last word: the trace kernel reads SVDAG headers as two
     // 16-B vectors that may extend up to 7 words past a node
     const uint64_t alloc_words = cursor + 8;
-    uint32_t* buf = nullptr;
-    cudaError_t e = cudaMalloc(&buf, alloc_words * sizeof(uint32_t));
-    if (e != cudaSuccess) {
-      set_error("vf_build: cudaMalloc(%llu bytes) failed: %s", (unsigned long long)(cursor * 4), cudaGetErrorString(e));
+    uint32_t* buf = static_cast<uint32_t*>(h->alloc.get(alloc_words * sizeof(uint32_t), s));
+    if (!buf) {
+      set_error("vf_build: allocation of the %llu-byte format buffer failed", (unsigned long long)(alloc_words * 4));
       return VF_ERR_OOM;
     }
+    h->buf = buf;  // owned by the handle from here on (freed by vf_build's error path / vf_destroy)
+    h->buf_bytes = alloc_words * sizeof(uint32_t);
     VF_CUDA_TRY(cudaMemsetAsync(buf, 0, alloc_words * sizeof(uint32_t), s));
     VF_CUDA_TRY(cudaMemcpyAsync(buf, &root, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
     for (uint32_t t = 0; t < f.n_tiers; ++t)

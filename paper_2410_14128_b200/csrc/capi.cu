@@ -31,8 +31,8 @@ struct DeviceGuard {
 
 extern "C" {
 
-vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_levels, uint32_t build_flags, int device,
-                   void* cuda_stream, vf_handle** out, uint64_t* bytes_used) {
+vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_levels, uint32_t build_flags,
+                   const vf_allocator* alloc, int device, void* cuda_stream, vf_handle** out, uint64_t* bytes_used) {
   clear_error();
   if (out) *out = nullptr;
   if (!vol || !levels || !out) {
@@ -49,6 +49,14 @@ vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_leve
   }
   if (vol->kind == VF_VOL_SPARSE_DEVICE && vol->n_voxels && (!vol->keys || !vol->values)) {
     set_error("vf_build: sparse volume without keys/values");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (alloc && (!alloc->alloc || !alloc->free)) {
+    set_error("vf_build: allocator needs both alloc and free");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (build_flags & ~(uint32_t)VF_BUILD_KNOWN_FLAGS) {
+    set_error("vf_build: unknown build flags 0x%x", build_flags & ~(uint32_t)VF_BUILD_KNOWN_FLAGS);
     return VF_ERR_INVALID_ARG;
   }
   Format f;
@@ -72,22 +80,29 @@ vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_leve
     return VF_ERR_OOM;
   }
   h->device = device;
+  if (alloc) h->alloc.a = *alloc;
+  h->build_stream = (cudaStream_t)cuda_stream;
   h->fmt = f;
   memset(&h->stats, 0, sizeof(h->stats));
   st = build_format(vol, f, build_flags, (cudaStream_t)cuda_stream, h);
   if (st != VF_OK) {
-    if (h->buf) cudaFree(h->buf);
+    if (h->buf) {
+      cudaStreamSynchronize(h->build_stream);
+      h->alloc.put(h->buf, h->buf_bytes, h->build_stream);
+    }
     delete h;
     return st;
   }
   h->tp = make_trace_params(f, h->stats.root);
   {
-    cudaError_t e = cudaMalloc(&h->work, sizeof(unsigned long long) * 2 * kWorkSlots);
-    if (e == cudaSuccess) e = cudaMemset(h->work, 0, sizeof(unsigned long long) * 2 * kWorkSlots);
+    const size_t wb = sizeof(unsigned long long) * 2 * kWorkSlots;
+    h->work = static_cast<unsigned long long*>(h->alloc.get(wb, h->build_stream));
+    cudaError_t e = h->work ? cudaMemsetAsync(h->work, 0, wb, h->build_stream) : cudaErrorMemoryAllocation;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->build_stream);
     if (e != cudaSuccess) {
       set_error("vf_build: work-counter allocation failed: %s", cudaGetErrorString(e));
-      if (h->work) cudaFree(h->work);
-      cudaFree(h->buf);
+      h->alloc.put(h->work, wb, h->build_stream);
+      h->alloc.put(h->buf, h->buf_bytes, h->build_stream);
       delete h;
       return VF_ERR_OOM;
     }
@@ -147,15 +162,16 @@ vf_status vf_trace_counters(const vf_handle* h, const vf_ray* rays, uint64_t n, 
   }
   DeviceGuard g(h->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  unsigned long long* d = nullptr;
-  VF_CUDA_TRY(cudaMalloc(&d, sizeof(unsigned long long) * VF_NCOUNTERS));
+  const size_t db = sizeof(unsigned long long) * VF_NCOUNTERS;
+  unsigned long long* d = static_cast<unsigned long long*>(h->alloc.get(db, s));
+  if (!d) {
+    set_error("vf_trace_counters: counter allocation failed");
+    return VF_ERR_OOM;
+  }
   // touch bitmap: one bit per format word (distinct words / sectors read by the frame)
   const uint64_t nbw = (h->n_words + 31) / 32;
-  uint32_t* touch = nullptr;
-  if (cudaMalloc(&touch, nbw * sizeof(uint32_t)) != cudaSuccess) {
-    cudaGetLastError();
-    touch = nullptr;  // too large to keep: the distinct-word counters stay 0
-  }
+  // (too large to keep: the distinct-word counters stay 0)
+  uint32_t* touch = static_cast<uint32_t*>(h->alloc.get(nbw * sizeof(uint32_t), s));
   unsigned long long ex = 0;
   vf_status st = read_exact_calls(&ex, true);
   if (st == VF_OK) {
@@ -177,8 +193,9 @@ vf_status vf_trace_counters(const vf_handle* h, const vf_ray* rays, uint64_t n, 
       counters[VF_CTR_EXACT_CALLS] = ex;
     }
   }
-  cudaFree(d);
-  if (touch) cudaFree(touch);
+  cudaStreamSynchronize(s);
+  h->alloc.put(d, db, s);
+  h->alloc.put(touch, nbw * sizeof(uint32_t), s);
   return st;
 }
 
@@ -200,12 +217,15 @@ vf_status vf_trace_host(vf_handle* h, const vf_ray* host_rays, uint64_t n, vf_hi
   const size_t rb = n * sizeof(vf_ray), hb = n * sizeof(vf_hit);
   const size_t need = ((rb + 255) & ~(size_t)255) + hb;
   if (h->stage_bytes < need) {
-    if (h->stage) cudaFree(h->stage);
+    if (h->stage) {
+      cudaDeviceSynchronize();  // the previous staging buffer may still be read by an earlier call's copies
+      h->alloc.put(h->stage, h->stage_bytes, h->build_stream);
+    }
     h->stage = nullptr;
     h->stage_bytes = 0;
-    cudaError_t e = cudaMalloc(&h->stage, need);
-    if (e != cudaSuccess) {
-      set_error("vf_trace_host: staging allocation of %zu bytes failed: %s", need, cudaGetErrorString(e));
+    h->stage = h->alloc.get(need, h->build_stream);
+    if (!h->stage) {
+      set_error("vf_trace_host: staging allocation of %zu bytes failed", need);
       return VF_ERR_OOM;
     }
     h->stage_bytes = need;
@@ -319,9 +339,10 @@ vf_status vf_buffer_read(const vf_handle* h, uint64_t first, uint64_t count, uin
 void vf_destroy(vf_handle* h) {
   if (!h) return;
   DeviceGuard g(h->device);
-  if (h->buf) cudaFree(h->buf);
-  if (h->stage) cudaFree(h->stage);
-  if (h->work) cudaFree(h->work);
+  cudaDeviceSynchronize();  // no kernel or copy of this handle may still use its memory
+  h->alloc.put(h->buf, h->buf_bytes, h->build_stream);
+  h->alloc.put(h->stage, h->stage_bytes, h->build_stream);
+  h->alloc.put(h->work, sizeof(unsigned long long) * 2 * kWorkSlots, h->build_stream);
   for (int i = 0; i < kPipe; ++i)
     if (h->pipe[i]) cudaStreamDestroy(h->pipe[i]);
   if (h->pipe_ev) cudaEventDestroy(h->pipe_ev);

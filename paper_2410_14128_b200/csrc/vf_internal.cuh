@@ -86,12 +86,41 @@ enum : uint32_t {
   TW_TOP = 1u << 30,     // first tier of its level
 };
 
+// Device memory of a handle and of its build (SURVEY.md §8(b) vf_allocator: "PyTorch only for
+// memory and streams"). a.alloc == NULL: cudaMalloc / cudaFree. Blocks are requested for, and
+// returned on, the stream of the call that uses them.
+struct DevAllocator {
+  vf_allocator a{};
+  void* get(size_t bytes, cudaStream_t s) const {
+    if (bytes == 0) bytes = 16;
+    if (a.alloc) return a.alloc(bytes, a.ctx, (void*)s);
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return p;
+  }
+  void put(void* p, size_t bytes, cudaStream_t s) const {
+    if (!p) return;
+    if (bytes == 0) bytes = 16;
+    if (a.alloc) {
+      if (a.free) a.free(p, bytes, a.ctx, (void*)s);
+    } else {
+      cudaFree(p);
+    }
+  }
+};
+
 struct Handle {
   int device = 0;
+  DevAllocator alloc;
+  cudaStream_t build_stream = nullptr;  // the buffer's allocation stream (returned there by vf_destroy)
   Format fmt;
   TraceParams tp;
   uint32_t* buf = nullptr;  // device words
   uint64_t n_words = 0;
+  size_t buf_bytes = 0;     // allocated bytes of buf (n_words + guard words)
   vf_stats stats{};
   // staging and pipeline streams for vf_trace_host
   void* stage = nullptr;

@@ -6,9 +6,11 @@ device memory and streams (tensors' data_ptr / torch.cuda.Stream.cuda_stream).
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 import re
+import weakref
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VF_LIB") or os.path.join(PKG, "libvf.so")  # VF_LIB: A/B builds (tools)
@@ -63,14 +65,40 @@ class Stats(ctypes.Structure):
 
 _vp = ctypes.c_void_p
 _u32, _u64 = ctypes.c_uint32, ctypes.c_uint64
+_ALLOC_FN = ctypes.CFUNCTYPE(_vp, ctypes.c_size_t, _vp, _vp)
+_FREE_FN = ctypes.CFUNCTYPE(None, _vp, ctypes.c_size_t, _vp, _vp)
+
+
+class Allocator(ctypes.Structure):  # vf_allocator
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", _vp)]
+
+
+def _torch_alloc(nbytes, ctx, stream):
+    """vf_allocator.alloc backed by torch's caching allocator (the device is the current one:
+    the library sets the handle's device around every call)."""
+    import torch
+    try:
+        return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(), stream or 0)
+    except Exception:  # out of memory: the library reports VF_ERR_OOM
+        return None
+
+
+def _torch_free(ptr, nbytes, ctx, stream):
+    import torch
+    torch.cuda.caching_allocator_delete(ptr)
+
+
+# kept alive for the life of the module (the library holds the function pointers until vf_destroy)
+_TORCH_ALLOC_FN, _TORCH_FREE_FN = _ALLOC_FN(_torch_alloc), _FREE_FN(_torch_free)
+TORCH_ALLOCATOR = Allocator(_TORCH_ALLOC_FN, _TORCH_FREE_FN, None)
 _sig = {
     "vf_last_error": ([], ctypes.c_char_p),
     "vf_abi_version": ([], ctypes.c_int),
     "vf_parse_format": ([ctypes.c_char_p, ctypes.POINTER(Level), _u32, ctypes.POINTER(_u32)], ctypes.c_int),
     "vf_format_to_string": ([ctypes.POINTER(Level), _u32, ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
     "vf_format_resolution": ([ctypes.POINTER(Level), _u32, ctypes.POINTER(_u32)], ctypes.c_int),
-    "vf_build": ([ctypes.POINTER(Volume), ctypes.POINTER(Level), _u32, _u32, ctypes.c_int, _vp, ctypes.POINTER(_vp),
-                  ctypes.POINTER(_u64)], ctypes.c_int),
+    "vf_build": ([ctypes.POINTER(Volume), ctypes.POINTER(Level), _u32, _u32, ctypes.POINTER(Allocator), ctypes.c_int,
+                  _vp, ctypes.POINTER(_vp), ctypes.POINTER(_u64)], ctypes.c_int),
     "vf_trace": ([_vp, _vp, _u64, _vp, _u32, _vp], ctypes.c_int),
     "vf_trace_host": ([_vp, _vp, _u64, _vp, _u32, _vp], ctypes.c_int),
     "vf_trace_ex": ([_vp, _vp, _u64, _vp, _vp, _u32, _vp], ctypes.c_int),
@@ -289,8 +317,22 @@ class Handle:
             pass
 
 
-def build(volume, signature, flags: int = VF_BUILD_DEFAULT, device: int | None = None, stream=None) -> Handle:
+_LIVE = weakref.WeakSet()  # handles closed at interpreter exit, while torch (their allocator) still works
+
+
+@atexit.register
+def _close_live_handles():
+    for h in list(_LIVE):
+        h.close()
+
+
+def build(volume, signature, flags: int = VF_BUILD_DEFAULT, device: int | None = None, stream=None,
+          allocator="torch") -> Handle:
     """Build a format.
+
+    allocator: "torch" (default) routes every device allocation of the build and of the handle
+            through torch's caching allocator (vf_allocator); None uses the library's cudaMalloc; an
+            Allocator instance is passed through as is.
 
     volume: a dense CUDA tensor (Rz, Ry, Rx) int32/uint32 RGBA (0 = empty), or a tuple
             (keys int64 CUDA tensor x|y<<21|z<<42, rgba int32 CUDA tensor, dims (Rx,Ry,Rz)).
@@ -320,6 +362,12 @@ def build(volume, signature, flags: int = VF_BUILD_DEFAULT, device: int | None =
         device = dev.index if dev.index is not None else torch.cuda.current_device()
     out = ctypes.c_void_p(0)
     used = _u64(0)
-    _check(_lib.vf_build(ctypes.byref(v), levels, len(levels), flags, device, _stream_ptr(stream), ctypes.byref(out),
-                         ctypes.byref(used)))
-    return Handle(out, sig, levels, used.value)
+    if isinstance(allocator, Allocator):  # a caller-supplied vf_allocator (kept alive by the caller)
+        alloc = ctypes.byref(allocator)
+    else:
+        alloc = ctypes.byref(TORCH_ALLOCATOR) if allocator == "torch" else None
+    _check(_lib.vf_build(ctypes.byref(v), levels, len(levels), flags, alloc, device, _stream_ptr(stream),
+                         ctypes.byref(out), ctypes.byref(used)))
+    h = Handle(out, sig, levels, used.value)
+    _LIVE.add(h)
+    return h

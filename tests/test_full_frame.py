@@ -80,6 +80,33 @@ def test_cfg4i_full_frame():
     _check("cfg4i", bench.SWEEP["cfg4i"], incoherent=True)
 
 
+def test_cfg4s_secondary_full_frame():
+    """SURVEY §8(f) NEXT 3 as specified: shadow + AO rays spawned from the cfg4 primary hits
+    (inputs.rays.secondary; origin on the entry face from the hit voxel / t / entry-face normal).
+    The spawn inputs are the ORACLE's primary hits (never the CUDA path's); every secondary ray of
+    the frame is traced on the GPU in bench.py's launch configuration (VF_TRACE_INCOHERENT hint)
+    and compared with the oracle, for every format of the cfg4s sweep, stack and restart."""
+    import bench
+    import torch
+    from inputs import rays as R
+    vol, prim, _, pref = _frame("cfg4")
+    rays, _src = R.secondary(prim, pref["xyz"], pref["t"], pref["normal"], seed=0x5EC1)
+    assert len(rays) > 1_000_000  # ~2 x the 56 % primary hit rate of 2,073,600 rays
+    g = oracle.Grid.from_generator(vol)
+    ref = g.trace(rays)
+    g.close()
+    assert (ref["status"] != 2).all()
+    shadow = ref["xyz"][: len(rays) // 2, 0] >= 0
+    assert 0.01 < shadow.mean() < 0.99  # both lit and shadowed points in the frame
+    rt = torch.from_numpy(rays).cuda()
+    hits = torch.empty((len(rays), 4), dtype=torch.int32, device="cuda")
+    for fmt, h in _handles(vol, bench.SWEEP["cfg4s"]):
+        for restart in (False, True):
+            h.trace(rt, hits, restart=restart, incoherent=True)
+            out = hits.cpu().numpy()
+            assert_parity(out[:, :3], out[:, 3].view(np.float32), ref, f"cfg4s {fmt} restart={restart} (full frame)")
+
+
 def test_cfg5_full_frame_every_sweep_format():
     """cfg5 (4096^3, 3840x2160 = 8,294,400 rays): the bench's headline R(4^3) G(8) and every other
     format of the cfg5 sweep, each over the whole frame, stack and restart."""
