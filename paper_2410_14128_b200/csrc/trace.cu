@@ -299,6 +299,8 @@ __device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, ui
 // (pure arithmetic in t; a packed compile-time table variant measured 2-8 % slower)
 struct NoSpec {
   static constexpr bool kStatic = false;
+  static constexpr int kLogDim = -1;  // log2 of the (cubic) resolution when compiled in; -1: p.dims
+  static constexpr bool kHasDF = true;  // some tier may be a DF grid
   static constexpr uint32_t kTopWords = 0;  // words of a stageable top Raw grid (0: none)
 };
 
@@ -313,6 +315,8 @@ struct TopSparse {
   __device__ static __forceinline__ bool df(int t) { return DFTOP && A > 0 && t == 0; }
   static constexpr int OFF = A > 0 ? 1 : 0;
   static constexpr int NT = (int)NS + OFF;
+  static constexpr int kLogDim = (int)(A + LF * NS);
+  static constexpr bool kHasDF = DFTOP;
   __device__ static __forceinline__ bool raw(int t) { return A > 0 && t == 0; }
   __device__ static __forceinline__ uint32_t lc(int t) { return LF * (uint32_t)(NT - 1 - t); }
   __device__ static __forceinline__ uint32_t msk(int t) { return raw(t) ? (1u << A) - 1u : (1u << LF) - 1u; }
@@ -341,6 +345,8 @@ struct RawChain {
   static constexpr bool kStatic = true;
   static constexpr uint32_t kTopWords = 0;
   static constexpr int NT = (int)(NR + NS);
+  static constexpr int kLogDim = (int)(A0 + (NR > 1 ? A1 : 0u) + (NR > 2 ? A2 : 0u) + NS);
+  static constexpr bool kHasDF = DFM != 0;
   static constexpr uint32_t L2 = NS, L1 = NS + (NR > 2 ? A2 : 0u), L0 = L1 + (NR > 1 ? A1 : 0u);  // lc of raw tiers
   __host__ __device__ static constexpr uint32_t LCR(int t) { return t == 0 ? (NR == 1 ? NS : NR == 2 ? NS + A1 : L0) : t == 1 ? (NR == 2 ? NS : L1) : L2; }
   __device__ static __forceinline__ bool raw(int t) { return t < (int)NR; }
@@ -379,6 +385,8 @@ struct TwoSparse {
   static constexpr int OFF = A > 0 ? 1 : 0;
   static constexpr int B = OFF + (int)N1;  // first tier of the second sparse level
   static constexpr int NT = B + (int)N2;
+  static constexpr int kLogDim = (int)(A + N1 + N2);
+  static constexpr bool kHasDF = false;
   __device__ static __forceinline__ bool raw(int t) { return A > 0 && t == 0; }
   __device__ static __forceinline__ uint32_t lc(int t) { return (uint32_t)(NT - 1 - t); }
   __device__ static __forceinline__ uint32_t msk(int t) { return raw(t) ? (1u << A) - 1u : 1u; }
@@ -405,6 +413,8 @@ struct SparseRaw {
   static constexpr uint32_t kTopWords = 0;
   __device__ static __forceinline__ bool df(int) { return false; }
   static constexpr uint32_t LC0 = LF * (NS - 1) + A;  // lc of tier 0
+  static constexpr int kLogDim = (int)(LF * NS + A);
+  static constexpr bool kHasDF = false;
   __device__ static __forceinline__ uint32_t lc(int t) { return t == (int)NS ? 0u : LC0 - LF * (uint32_t)t; }
   __device__ static __forceinline__ uint32_t msk(int t) { return t == (int)NS ? (1u << A) - 1u : (1u << LF) - 1u; }
   __device__ static __forceinline__ uint32_t sx(int t) { return t == (int)NS ? A : LF; }
@@ -742,15 +752,32 @@ struct Lane {
       // voxel of the stale axes within the parent cell (edge 2^lc(t-1); bits above it exact).
       // (never true after a pop: a pop lands on a tier with lc() >= stale_lc)
       if (stale && lc() < stale_lc) {
-        const uint32_t pl = lcp();
         const int st = stale & moving;
+        // fast path of locate() on every stale axis at once (predicated, no per-axis branch):
+        // x^ = fma(T^_E, d_b, o_b) is certified to lie strictly inside a cell unless it is within
+        // B of an integer; those axes (a ray on / near a plane at E) take the certified slow path
+        int slow = 0;
 #pragma unroll
-        for (int b = 0; b < 3; ++b)
-          if ((st >> b) & 1) {
-            const int lo = (V[b] >> pl) << pl;
-            V[b] = locate(b, lo, lo + (1 << pl) - 1);
-            ct.add(VF_CTR_LOCATES);
-          }
+        for (int b = 0; b < 3; ++b) {
+          const float x = fmaf(et, d[b], o[b]);
+          const float fl = floorf(x);
+          const float f = x - fl;  // exact
+          const float B = (fabsf(et * d[b]) + fabsf(x)) * 0x1p-21f;
+          const bool ok = f > B && 1.0f - f > B;
+          const bool sb = (st >> b) & 1;
+          if (sb && ok) V[b] = (int)fl;
+          slow |= (sb && !ok) ? 1 << b : 0;
+        }
+        ct.add(VF_CTR_LOCATES, __popc(st));
+        if (slow) {
+          const uint32_t pl = lcp();
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            if ((slow >> b) & 1) {
+              const int lo = (V[b] >> pl) << pl;
+              V[b] = locate(b, lo, lo + (1 << pl) - 1);
+            }
+        }
         stale = 0;
         stale_lc = 0;
       }
@@ -760,35 +787,39 @@ struct Lane {
 
   // -- step: exact next event among the three axes at this tier's cell size. Sets nt < 0 when
   // the segment ends (miss), nt < t (with nN) when the step leaves the current node.
+  // (Instruction-lean form: the cell's next plane is its low corner, plus the cell edge for
+  //  d > 0; only the stepped axes' cells change, so the root-box test and the changed-bit mask
+  //  need no per-axis selects, and with a compiled-in cubic resolution 2^K the root-box test is
+  //  one shift of the OR of the three coordinates.)
   __device__ __forceinline__ void step(const TraceParams& p, uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct, int& nt,
                                        uint32_t& nN) {
     ct.add(VF_CTR_STEPS);
+    const uint32_t l = lc();
+    const int cell = 1 << l;
     int Pn[3];
     float tn[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       // next plane on axis a at this tier's cell size (inv = +inf makes a d = 0 axis never step)
-      Pn[a] = ((V[a] >> lc()) + 1 - ((dneg >> a) & 1)) << lc();
+      const int lo = V[a] & -cell;
+      Pn[a] = ((dneg >> a) & 1) ? lo : lo + cell;
       tn[a] = tplane(Pn[a], o[a], inv[a]);
     }
     const float m = fminf(fminf(tn[0], tn[1]), tn[2]);
     const float thr = fmaf(fabsf(m), kCertEps, m);  // m + |m| eps: also for m < 0 (tmin < 0)
-    // s[a]: axis a steps. One candidate within the certification margin of the fp32 minimum is
+    // S: the stepping axes. One candidate within the certification margin of the fp32 minimum is
     // certified to be the exact minimum; several go to the exact argmin (ties step together).
-    bool s[3] = {tn[0] <= thr, tn[1] <= thr, tn[2] <= thr};
-    int S = (s[0] ? 1 : 0) | (s[1] ? 2 : 0) | (s[2] ? 4 : 0);
+    int S = (tn[0] <= thr ? 1 : 0) | (tn[1] <= thr ? 2 : 0) | (tn[2] <= thr ? 4 : 0);
     if (S == 0) {  // no finite next event (non-finite ray data outside the domain): end the walk
       nt = -1;
       return;
     }
     if ((S & (S - 1)) == 0) {
-      eaxis = s[0] ? 0 : (s[1] ? 1 : 2);
+      eaxis = __ffs(S) - 1;
       et = m;
     } else {
       const int res = argmin_exact(o[0], o[1], o[2], d[0], d[1], d[2], Pn[0], Pn[1], Pn[2], tn[0], tn[1], tn[2], S);
       S = res & 7;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) s[a] = (res >> a) & 1;
       eaxis = res >> 4;
       et = sel3(tn, eaxis);
       ct.add(VF_CTR_NEAR_TIES);
@@ -796,14 +827,17 @@ struct Lane {
     // every axis of S steps into the cell adjacent to its plane (exact ties together, reading A2);
     // V is updated in place (on a miss it is not used again)
     int x = 0;
+    uint32_t vor = 0;
     bool out_of_box = false;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const int nv = Pn[a] - ((dneg >> a) & 1);
-      out_of_box |= s[a] && (uint32_t)nv >= (uint32_t)p.dims[a];
-      x |= s[a] ? (nv ^ V[a]) : 0;
-      V[a] = s[a] ? nv : V[a];
+      const int nv = ((S >> a) & 1) ? Pn[a] - ((dneg >> a) & 1) : V[a];
+      x |= nv ^ V[a];
+      V[a] = nv;
+      vor |= (uint32_t)nv;
+      if constexpr (D::kLogDim < 0) out_of_box |= (uint32_t)nv >= (uint32_t)p.dims[a];
     }
+    if constexpr (D::kLogDim >= 0) out_of_box = (vor >> D::kLogDim) != 0u;
     if (out_of_box) {  // left the root box
       nt = -1;
       return;
@@ -813,13 +847,16 @@ struct Lane {
       nt = -1;
       return;
     }
-    // (axes with d = 0 may be marked too: they never move, and the locate block skips them)
-    if (lc()) {
-      stale |= ~S & 7;
-      stale_lc = max(stale_lc, lc());
+    // bits of V below l on the non-stepped axes are stale from here on (axes with d = 0 may be
+    // marked too: they never move, and the locate block skips them)
+    if (l) {
+      stale = ~S & 7;  // (stale was a subset of the three axes)
+      stale_lc = max(stale_lc, l);
+    } else {
+      stale &= ~S;
     }
-    stale &= ~S;
-    budget -= __popc(S);  // L1 distance moved (DF tiers only use it)
+    if constexpr (!SPEC) budget -= __popc(S);  // L1 distance moved (DF tiers only use it)
+    else if (D::kHasDF) budget -= __popc(S);
     // h = highest bit in which the old and new cells differ; the step leaves this tier's node iff
     // h >= lc(t-1) (the node's edge), and then tau(h) is the deepest tier whose node holds both
     const uint32_t h = 31u - __clz((uint32_t)x);

@@ -67,8 +67,10 @@ def test_torch_allocator_owns_the_handle_memory():
     the buffer and the trace are identical to a build with the library's cudaMalloc."""
     import torch
     from paper_2410_14128_b200 import vf
+    from inputs import rays as R
     d = inputs.menger(128, 4)
     keys, rgba = inputs.voxels_device(d)
+    rays = torch.from_numpy(R.perspective(64, 64, 60.0, (-40.3, 60.7, -70.1), (40.5, 40.5, 40.5))[0]).cuda()
     torch.cuda.synchronize()
     before = torch.cuda.memory_allocated()
     ht = vf.build((keys, rgba, (128,) * 3), "R(3^3) G(4)")
@@ -79,8 +81,6 @@ def test_torch_allocator_owns_the_handle_memory():
     assert torch.cuda.memory_allocated() - before == held  # cudaMalloc: invisible to torch
     assert ht.bytes_used == hc.bytes_used
     assert np.array_equal(ht.buffer_words(), hc.buffer_words())
-    from inputs import rays as R
-    rays = torch.from_numpy(R.perspective(64, 64, 60.0, (-40.3, 60.7, -70.1), (40.5, 40.5, 40.5))[0]).cuda()
     assert torch.equal(ht.trace(rays), hc.trace(rays))
     ht.close()
     hc.close()
