@@ -504,6 +504,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{cfg}: {desc}", "format": handle.signature,
                        "variant": ("restart" if args.restart else "stack") + ("+incoherent" if incoh else ""),
+                       "kernel": "compiled-in" if stats.get("compiled_in") else "generic",
                        "volume": list(dims), "rays_per_frame": n_total, "nonempty_voxels": nonempty,
                        "bytes_used": stats["bytes_used"], "bytes_per_voxel": round(stats["bytes_used"] / nonempty, 4),
                        "bytes_per_voxel_paper": round(stats["paper_layout_bytes"] / nonempty, 4),
@@ -581,6 +582,7 @@ def sweep(cfg, vol, rays, hits, stream, flush, args):
             o = hits[:n].cpu().numpy()
             nb, _ = compare(o[idx, :3], o[idx, 3].view(np.float32), ref)
             out.append({"format": h.signature, "variant": "restart" if restart else "stack",
+                        "kernel": "compiled-in" if st.get("compiled_in") else "generic",
                         "mrays_s": round(n / (t_ms / 1e3) / 1e6, 1),
                         "bytes_per_voxel": round(st["bytes_used"] / st["nonempty_voxels"], 4),
                         "paper_bytes_per_voxel": round(st["paper_layout_bytes"] / st["nonempty_voxels"], 4),

@@ -272,6 +272,10 @@ typedef struct {
   uint64_t words_per_tier[VF_MAX_TIERS]; /* paper-layout words written by each tier */
   uint64_t dedup_leaf_nodes;   /* SVDAG 1-word leaf nodes stored (all SVDAG levels) */
   double build_ms;             /* wall time of vf_build */
+  uint32_t compiled_in;        /* 1: vf_trace runs a kernel with this format compiled in (the
+                                  paper's per-format generated code, §4, as a template instance);
+                                  0: the generic tier-table kernel */
+  uint32_t reserved_;
 } vf_stats;
 
 VF_API vf_status vf_stats_get(const vf_handle* h, vf_stats* out);

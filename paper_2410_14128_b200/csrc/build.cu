@@ -540,14 +540,15 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
     uint64_t paper_words = 1;
     uint32_t root = 0;
 
-    // Stored offsets are u32 word addresses (16 GiB limit; reading A15): every node of
-    // a tier below the root is referenced by one, so it must end below 2^32 words; the root tier is
-    // referenced only by word 0 (its base). A single Raw level stores no offsets (64-bit indexing).
-    // Checked before a tier's words are allocated, so an oversized plan fails fast.
+    // Stored offsets are u32 word addresses (16 GiB limit; reading A15): every node is
+    // referenced by one (the root by word 0), and the trace kernels address cells of multi-tier
+    // buffers in 32 bits, so every tier must end at or below word 2^32. A single Raw level stores no
+    // offsets (64-bit indexing). Checked before a tier's words are allocated: an oversized plan
+    // fails fast.
     const bool single_raw = f.n_tiers == 1 && f.tiers[0].kind == K_RAW;
     auto offsets_fit = [&](int t, uint64_t base, uint64_t words) {
       if (single_raw) return true;
-      if (t == 0 ? base < (1ull << 32) : base + words <= (1ull << 32)) return true;
+      if (base + words <= (1ull << 32)) return true;
       set_error("vf_build: tier %d needs words [%llu, %llu); stored offsets must stay below 2^32 words "
                 "(16 GiB, PAPER.md:86)", t, (unsigned long long)base, (unsigned long long)(base + words));
       return false;

@@ -109,6 +109,7 @@ vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_leve
   }
   for (int a = 0; a < 3; ++a) h->stats.dims[a] = f.dims[a];
   h->stats.n_levels = f.n_levels;
+  h->stats.compiled_in = has_compiled_in_kernel(f) ? 1u : 0u;
   h->stats.n_tiers = f.n_tiers;
   if (bytes_used) *bytes_used = h->stats.bytes_used;
   *out = h;

@@ -47,6 +47,17 @@ namespace {
 constexpr float kCertEps = 0x1p-20f;  // certification margin (>= 8u with u = 2^-24; see header)
 constexpr int TMIN_AXIS = 3;
 
+// One thread per ray, 128-thread blocks; register caps (__launch_bounds__ min blocks per SM)
+#ifndef VF_MINB
+#define VF_MINB 8  // __launch_bounds__ min blocks per SM (register cap), A/B-tuned
+#endif
+#ifndef VF_MINB_SPEC
+#define VF_MINB_SPEC 9  // compiled-in formats: 56 registers, 9 blocks per SM (A/B: +1.4-2.2 % over 8)
+#endif
+#ifndef VF_MINB_CHAIN
+#define VF_MINB_CHAIN 8  // compiled-in chains of several Raw / DF levels
+#endif
+
 struct Ray {
   float o[3], d[3], inv[3];
   float tmin, tmax;
@@ -301,6 +312,10 @@ struct NoSpec {
   static constexpr bool kStatic = false;
   static constexpr int kLogDim = -1;  // log2 of the (cubic) resolution when compiled in; -1: p.dims
   static constexpr bool kHasDF = true;  // some tier may be a DF grid
+  static constexpr int kMinBlocks = VF_MINB;  // __launch_bounds__ min blocks per SM (register cap)
+  static constexpr bool kIdx64 = true;        // Raw cell addresses may reach 2^32 words
+  static constexpr bool kCacheGeom = false;   // compiled-in tier geometry cached in registers
+  static constexpr bool kChainRestart = true; // restart variant: descents chained before each step
   static constexpr uint32_t kTopWords = 0;  // words of a stageable top Raw grid (0: none)
 };
 
@@ -317,6 +332,10 @@ struct TopSparse {
   static constexpr int NT = (int)NS + OFF;
   static constexpr int kLogDim = (int)(A + LF * NS);
   static constexpr bool kHasDF = DFTOP;
+  static constexpr int kMinBlocks = VF_MINB_SPEC;
+  static constexpr bool kIdx64 = false;
+  static constexpr bool kCacheGeom = false;
+  static constexpr bool kChainRestart = true;
   __device__ static __forceinline__ bool raw(int t) { return A > 0 && t == 0; }
   __device__ static __forceinline__ uint32_t lc(int t) { return LF * (uint32_t)(NT - 1 - t); }
   __device__ static __forceinline__ uint32_t msk(int t) { return raw(t) ? (1u << A) - 1u : (1u << LF) - 1u; }
@@ -347,6 +366,15 @@ struct RawChain {
   static constexpr int NT = (int)(NR + NS);
   static constexpr int kLogDim = (int)(A0 + (NR > 1 ? A1 : 0u) + (NR > 2 ? A2 : 0u) + NS);
   static constexpr bool kHasDF = DFM != 0;
+  // several Raw / DF tiers keep more geometry live: a looser register cap (A/B: VF_MINB_CHAIN)
+  static constexpr int kMinBlocks = NR > 1 ? VF_MINB_CHAIN : VF_MINB_SPEC;
+  static constexpr bool kIdx64 = NR == 1 && NS == 0 && A0 >= 10;  // a single grid of 2^30+ cells
+  // several Raw tiers: their geometry is a chain of selects on t; cache it per tier change instead
+#ifndef VF_CHAIN_CACHE
+#define VF_CHAIN_CACHE 1
+#endif
+  static constexpr bool kCacheGeom = NR > 1 && VF_CHAIN_CACHE;
+  static constexpr bool kChainRestart = NS > 0;  // only Raw levels: nothing to re-descend
   static constexpr uint32_t L2 = NS, L1 = NS + (NR > 2 ? A2 : 0u), L0 = L1 + (NR > 1 ? A1 : 0u);  // lc of raw tiers
   __host__ __device__ static constexpr uint32_t LCR(int t) { return t == 0 ? (NR == 1 ? NS : NR == 2 ? NS + A1 : L0) : t == 1 ? (NR == 2 ? NS : L1) : L2; }
   __device__ static __forceinline__ bool raw(int t) { return t < (int)NR; }
@@ -387,6 +415,10 @@ struct TwoSparse {
   static constexpr int NT = B + (int)N2;
   static constexpr int kLogDim = (int)(A + N1 + N2);
   static constexpr bool kHasDF = false;
+  static constexpr int kMinBlocks = VF_MINB_SPEC;
+  static constexpr bool kIdx64 = false;
+  static constexpr bool kCacheGeom = false;
+  static constexpr bool kChainRestart = true;
   __device__ static __forceinline__ bool raw(int t) { return A > 0 && t == 0; }
   __device__ static __forceinline__ uint32_t lc(int t) { return (uint32_t)(NT - 1 - t); }
   __device__ static __forceinline__ uint32_t msk(int t) { return raw(t) ? (1u << A) - 1u : 1u; }
@@ -415,6 +447,10 @@ struct SparseRaw {
   static constexpr uint32_t LC0 = LF * (NS - 1) + A;  // lc of tier 0
   static constexpr int kLogDim = (int)(LF * NS + A);
   static constexpr bool kHasDF = false;
+  static constexpr int kMinBlocks = VF_MINB_SPEC;
+  static constexpr bool kIdx64 = false;
+  static constexpr bool kCacheGeom = false;
+  static constexpr bool kChainRestart = true;
   __device__ static __forceinline__ uint32_t lc(int t) { return t == (int)NS ? 0u : LC0 - LF * (uint32_t)t; }
   __device__ static __forceinline__ uint32_t msk(int t) { return t == (int)NS ? (1u << A) - 1u : (1u << LF) - 1u; }
   __device__ static __forceinline__ uint32_t sx(int t) { return t == (int)NS ? A : LF; }
@@ -472,16 +508,16 @@ struct Lane {
 
   // tier geometry and flags of tier t
   __device__ __forceinline__ uint32_t lc() const {
-    if constexpr (SPEC) return D::lc(t); else return lc_;
+    if constexpr (SPEC && !D::kCacheGeom) return D::lc(t); else return lc_;
   }
   __device__ __forceinline__ uint32_t msk() const {
-    if constexpr (SPEC) return D::msk(t); else return msk_;
+    if constexpr (SPEC && !D::kCacheGeom) return D::msk(t); else return msk_;
   }
   __device__ __forceinline__ uint32_t sx() const {
-    if constexpr (SPEC) return D::sx(t); else return sx_;
+    if constexpr (SPEC && !D::kCacheGeom) return D::sx(t); else return sx_;
   }
   __device__ __forceinline__ uint32_t sxy() const {
-    if constexpr (SPEC) return D::sxy(t); else return sxy_;
+    if constexpr (SPEC && !D::kCacheGeom) return D::sxy(t); else return sxy_;
   }
   __device__ __forceinline__ uint32_t kind() const {
     if constexpr (SPEC) return D::kind(t); else return tw & 3u;
@@ -579,6 +615,11 @@ struct Lane {
       msk_ = a.z;
       sx_ = a.w;
       sxy_ = s_tw[8 * nt + 4];
+    } else if constexpr (D::kCacheGeom) {  // compiled-in, but cached in registers per tier change
+      lc_ = D::lc(nt);
+      msk_ = D::msk(nt);
+      sx_ = D::sx(nt);
+      sxy_ = D::sxy(nt);
     }
     budget = 0;
   }
@@ -668,70 +709,149 @@ struct Lane {
   // Invariant: V >> lc() is the current (untested) cell of node N at tier t, entered at E (the
   // tier-change block below re-derives stale sub-cell bits right after a descent).
   // A pop always follows a step, so it lands on a new cell.
-  __device__ __forceinline__ int iterate(const TraceParams& p, const uint32_t* __restrict__ buf,
-                                         const uint32_t* s_tw, uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
-    int nt = t;       // tier after this iteration
-    uint32_t nN = N;  // node after this iteration
+  // -- test the current cell of the current node (ordered_hit_children, one child): occ, and for
+  // an occupied cell above the finest tier its child (next node, or the next level's root)
+  __device__ __forceinline__ void test_cell(const uint32_t* __restrict__ buf, Ctr<COUNT>& ct, bool& occ,
+                                            uint32_t& child) {
     const uint32_t kind = this->kind();
     const bool finest = this->finest();
-    {
-      // -- test the current cell of the current node (ordered_hit_children, one child)
-      const uint32_t lx = ((uint32_t)V[0] >> lc()) & msk(), ly = ((uint32_t)V[1] >> lc()) & msk(),
-                     lz = ((uint32_t)V[2] >> lc()) & msk();
-      bool occ = false;
-      uint32_t child = 0;
-      ct.add(VF_CTR_CELL_TESTS);
-      if (has_kind<KINDS>(K_RAW) && kind == K_RAW) {
-        // 64-bit index: a single-level R(11^3) grid has 2^33 cells (reading A15)
-        const size_t lin = (size_t)lx + ((size_t)ly << sx()) + ((size_t)lz << sxy());
-        if (!is_df()) {
-          if constexpr (STAGE) child = t == 0 ? s_top[lin] : __ldg(buf + (size_t)N + lin);
-          else child = __ldg(buf + (size_t)N + lin);
-          occ = child != 0u;
-          ct.add(VF_CTR_RAW_CELLS);
-          ct.add(VF_CTR_FORMAT_BYTES, 4);
-          ct.touch((size_t)N + lin, 1);
-        } else if (budget > 0) {
-          // DF: within L1 distance `budget` of a cell whose nearest non-empty cell is that far
-          // away, so empty without a memory access ("how many voxels can be
-          // marched through before checking occupancy")
-          ct.add(VF_CTR_DF_SKIPS);
-        } else {
-          const uint2 v = __ldg(reinterpret_cast<const uint2*>(buf + (size_t)N + 2 * lin));
-          child = v.x;
-          occ = child != 0u;
-          budget = (int)v.y;
-          ct.add(VF_CTR_RAW_CELLS);
-          ct.add(VF_CTR_FORMAT_BYTES, 8);
-          ct.touch((size_t)N + 2 * lin, 2);
-        }
+    occ = false;
+    child = 0;
+    const uint32_t lx = ((uint32_t)V[0] >> lc()) & msk(), ly = ((uint32_t)V[1] >> lc()) & msk(),
+                   lz = ((uint32_t)V[2] >> lc()) & msk();
+    ct.add(VF_CTR_CELL_TESTS);
+    if (has_kind<KINDS>(K_RAW) && kind == K_RAW) {
+      // 64-bit index only where a grid can reach 2^32 words: a single-level R(11^3) grid has 2^33
+      // cells (reading A15); every tier of a multi-tier buffer ends below word 2^32 (vf_build)
+      using Idx = typename std::conditional<D::kIdx64, size_t, uint32_t>::type;
+      const Idx lin = (Idx)lx + ((Idx)ly << sx()) + ((Idx)lz << sxy());
+      if (!is_df()) {
+        if constexpr (STAGE) child = t == 0 ? s_top[lin] : __ldg(buf + ((Idx)N + lin));
+        else child = __ldg(buf + ((Idx)N + lin));
+        occ = child != 0u;
+        ct.add(VF_CTR_RAW_CELLS);
+        ct.add(VF_CTR_FORMAT_BYTES, 4);
+        ct.touch((size_t)N + lin, 1);
+      } else if (budget > 0) {
+        // DF: within L1 distance `budget` of a cell whose nearest non-empty cell is that far
+        // away, so empty without a memory access ("how many voxels can be
+        // marched through before checking occupancy")
+        ct.add(VF_CTR_DF_SKIPS);
       } else {
-        const uint32_t lin = lx + (ly << sx()) + (lz << sxy());
-        occ = (hd.mask >> lin) & 1u;
-        if (occ && !finest) {
-          const uint32_t rank = hd.rank(lin);
-          const bool last = this->last();
-          if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
-            child = hd.base + 2u * rank;
-          } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-            child = __ldg(buf + N + 1u + rank);
-            ct.add(VF_CTR_SVDAG_PTRS);
-            ct.add(VF_CTR_FORMAT_BYTES, 4);
-            ct.touch(N + 1u + rank, 1);
-          } else {
-            child = hd.base + (last ? 1u : 4u) * rank;
-          }
-          if (last) {  // leaf TermInt -> next level's root
-            ct.touch(child, 1);
-            child = __ldg(buf + child);
-            ct.add(VF_CTR_LEAF_WORDS);
-            ct.add(VF_CTR_FORMAT_BYTES, 4);
-          }
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(buf + ((Idx)N + 2 * lin)));
+        child = v.x;
+        occ = child != 0u;
+        budget = (int)v.y;
+        ct.add(VF_CTR_RAW_CELLS);
+        ct.add(VF_CTR_FORMAT_BYTES, 8);
+        ct.touch((size_t)N + 2 * lin, 2);
+      }
+    } else {
+      const uint32_t lin = lx + (ly << sx()) + (lz << sxy());
+      occ = (hd.mask >> lin) & 1u;
+      if (occ && !finest) {
+        const uint32_t rank = hd.rank(lin);
+        const bool last = this->last();
+        if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
+          child = hd.base + 2u * rank;
+        } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
+          child = __ldg(buf + N + 1u + rank);
+          ct.add(VF_CTR_SVDAG_PTRS);
+          ct.add(VF_CTR_FORMAT_BYTES, 4);
+          ct.touch(N + 1u + rank, 1);
+        } else {
+          child = hd.base + (last ? 1u : 4u) * rank;
+        }
+        if (last) {  // leaf TermInt -> next level's root
+          ct.touch(child, 1);
+          child = __ldg(buf + child);
+          ct.add(VF_CTR_LEAF_WORDS);
+          ct.add(VF_CTR_FORMAT_BYTES, 4);
         }
       }
+    }
+  }
+
+  // -- tier change: enter node nN at tier nt (descent or pop): its header, and after a descent
+  // the exact sub-cell of every stale axis
+  __device__ __forceinline__ void enter(const uint32_t* __restrict__ buf, const uint32_t* s_tw, Ctr<COUNT>& ct,
+                                        int nt, uint32_t nN) {
+    set_tier(s_tw, nt);
+    N = nN;
+    load_header<KINDS>(buf, this->kind(), N, hd, ct);
+    // after a descent, the new tier's cell needs V's bits >= lc(); if some of those are stale (the
+    // ray moved inside a cell of size 2^stale_lc since they were exact), derive the exact finest
+    // voxel of the stale axes within the parent cell (edge 2^lc(t-1); bits above it exact).
+    // (never true after a pop: a pop lands on a tier with lc() >= stale_lc)
+    if (stale && lc() < stale_lc) {
+      const int st = stale & moving;
+      // fast path of locate() on every stale axis at once (predicated, no per-axis branch):
+      // x^ = fma(T^_E, d_b, o_b) is certified to lie strictly inside a cell unless it is within
+      // B of an integer; those axes (a ray on / near a plane at E) take the certified slow path
+      int slow = 0;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const float x = fmaf(et, d[b], o[b]);
+        const float fl = floorf(x);
+        const float f = x - fl;  // exact
+        const float B = (fabsf(et * d[b]) + fabsf(x)) * 0x1p-21f;
+        const bool ok = f > B && 1.0f - f > B;
+        const bool sb = (st >> b) & 1;
+        if (sb && ok) V[b] = (int)fl;
+        slow |= (sb && !ok) ? 1 << b : 0;
+      }
+      ct.add(VF_CTR_LOCATES, __popc(st));
+      if (slow) {
+        const uint32_t pl = lcp();
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          if ((slow >> b) & 1) {
+            const int lo = (V[b] >> pl) << pl;
+            V[b] = locate(b, lo, lo + (1 << pl) - 1);
+          }
+      }
+      stale = 0;
+      stale_lc = 0;
+    }
+  }
+
+  __device__ __forceinline__ int iterate(const TraceParams& p, const uint32_t* __restrict__ buf,
+                                         const uint32_t* s_tw, uint32_t (&stk)[VF_MAX_TIERS], Ctr<COUNT>& ct) {
+#ifndef VF_DESCEND_CHAIN_STACK
+    constexpr bool kChain = RESTART && D::kChainRestart;
+#else
+    constexpr bool kChain = true;
+#endif
+    if constexpr (kChain) {
+    // Restart variant: one DDA step per iteration, preceded by the chain of descents into occupied
+    // cells (a restart re-descends several tiers at once; A/B: restart +2-9 %, stack -5-+0.4 %)
+    for (;;) {
+      bool occ;
+      uint32_t child;
+      test_cell(buf, ct, occ, child);
+      if (!occ) break;
+      if (finest()) return IT_HIT;  // unit intersection
+      if (!RESTART || is_top()) stk[t] = N;
+      ct.add(VF_CTR_DESCENTS);
+      enter(buf, s_tw, ct, t + 1, child);
+    }
+    int nt = t;
+    uint32_t nN = N;
+    step(p, stk, ct, nt, nN);
+    if (nt < 0) return IT_MISS;
+    if (nt != t) enter(buf, s_tw, ct, nt, nN);  // pop
+    return IT_CONTINUE;
+    } else {
+    // Stack variant: one cell test per iteration, followed by either a descent or a DDA step
+    int nt = t;       // tier after this iteration
+    uint32_t nN = N;  // node after this iteration
+    {
+      bool occ;
+      uint32_t child;
+      test_cell(buf, ct, occ, child);
       if (occ) {
-        if (finest) return IT_HIT;  // unit intersection
-        // descend at event E (the child's entry cell is derived at the top of the next iteration)
+        if (finest()) return IT_HIT;  // unit intersection
+        // descend at event E (the child's entry cell is derived in the tier change below)
         if (!RESTART || is_top()) stk[t] = N;
         nt = t + 1;
         nN = child;
@@ -743,46 +863,9 @@ struct Lane {
       if (nt < 0) return IT_MISS;
     }
     // tier change (descent or pop), shared by both paths so a warp mixing them runs it once
-    if (nt != t) {
-      set_tier(s_tw, nt);
-      N = nN;
-      load_header<KINDS>(buf, this->kind(), N, hd, ct);
-      // after a descent, the new tier's cell needs V's bits >= lc(); if some of those are stale (the
-      // ray moved inside a cell of size 2^stale_lc since they were exact), derive the exact finest
-      // voxel of the stale axes within the parent cell (edge 2^lc(t-1); bits above it exact).
-      // (never true after a pop: a pop lands on a tier with lc() >= stale_lc)
-      if (stale && lc() < stale_lc) {
-        const int st = stale & moving;
-        // fast path of locate() on every stale axis at once (predicated, no per-axis branch):
-        // x^ = fma(T^_E, d_b, o_b) is certified to lie strictly inside a cell unless it is within
-        // B of an integer; those axes (a ray on / near a plane at E) take the certified slow path
-        int slow = 0;
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const float x = fmaf(et, d[b], o[b]);
-          const float fl = floorf(x);
-          const float f = x - fl;  // exact
-          const float B = (fabsf(et * d[b]) + fabsf(x)) * 0x1p-21f;
-          const bool ok = f > B && 1.0f - f > B;
-          const bool sb = (st >> b) & 1;
-          if (sb && ok) V[b] = (int)fl;
-          slow |= (sb && !ok) ? 1 << b : 0;
-        }
-        ct.add(VF_CTR_LOCATES, __popc(st));
-        if (slow) {
-          const uint32_t pl = lcp();
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-            if ((slow >> b) & 1) {
-              const int lo = (V[b] >> pl) << pl;
-              V[b] = locate(b, lo, lo + (1 << pl) - 1);
-            }
-        }
-        stale = 0;
-        stale_lc = 0;
-      }
-    }
+    if (nt != t) enter(buf, s_tw, ct, nt, nN);
     return IT_CONTINUE;
+    }
   }
 
   // -- step: exact next event among the three axes at this tier's cell size. Sets nt < 0 when
@@ -929,18 +1012,12 @@ __device__ __forceinline__ void stage_tiers(const TraceParams& p, uint32_t* s_tw
 }
 
 // One thread per ray, 128-thread blocks.
-#ifndef VF_MINB
-#define VF_MINB 8  // __launch_bounds__ min blocks per SM (register cap), A/B-tuned
-#endif
-#ifndef VF_MINB_SPEC
-#define VF_MINB_SPEC 9  // compiled-in formats: 56 registers, 9 blocks per SM (A/B: +1.4-2.2 % over 8)
-#endif
 #ifndef VF_TRACE_THREADS
 #define VF_TRACE_THREADS 128  // block size (A/B: 256 with VF_MINB 4 keeps the 64-register cap)
 #endif
 constexpr unsigned kTraceThreads = VF_TRACE_THREADS;
 template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec>
-__global__ void __launch_bounds__(kTraceThreads, D::kStatic ? VF_MINB_SPEC : VF_MINB) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
+__global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
                                                     uint64_t n, unsigned long long* __restrict__ counters,
                                                     unsigned long long* __restrict__ work) {
@@ -1057,7 +1134,7 @@ __global__ void __launch_bounds__(kPersistThreads, VF_PMINB) trace_persistent(co
 // the in-warp tail of finished lanes. STAGE: the top Raw grid (<= 16 KB) is copied to shared memory
 // once per block and tier-0 cell tests read it there. work[0] = next ray, work[1] = finished blocks.
 template <uint32_t KINDS, bool RESTART, class D, bool STAGE>
-__global__ void __launch_bounds__(kTraceThreads, D::kStatic ? VF_MINB_SPEC : VF_MINB)
+__global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks)
     trace_chunked(const TraceParams p, const uint32_t* __restrict__ buf, const float4* __restrict__ rays,
                   int4* __restrict__ hits, uint64_t n, unsigned long long* __restrict__ counters,
                   unsigned long long* __restrict__ work) {
@@ -1391,11 +1468,18 @@ KernelFn select_spec(const Format& f, bool restart, int mode) {
 #define VF_RC(nr, a0, a1, a2, dfm, k, ns, kinds) \
   case ((nr) << 28) | ((a0) << 24) | ((a1) << 20) | ((a2) << 16) | ((dfm) << 12) | ((k) << 8) | (ns): \
     return spec_kernel<kinds, RawChain<nr, a0, a1, a2, dfm, K_OF_##k, ns>>(restart, mode);
-      // single Raw / DF grids (cfg4 R(11^3), t512 R(9^3) / D(9^3, 6), cfg2 R(8^3), cfg1 R(6^3)); the
-      // multi-level chains measured 1-13 % slower than the generic kernel and are not instantiated
+      // single Raw / DF grids (cfg4 R(11^3), t512 R(9^3) / D(9^3, 6), cfg2 R(8^3), cfg1 R(6^3))
       VF_RC(1, 11, 0, 0, 0, VF_NONE, 0, 1) VF_RC(1, 9, 0, 0, 0, VF_NONE, 0, 1) VF_RC(1, 9, 0, 0, 1, VF_NONE, 0, 1)
       VF_RC(1, 8, 0, 0, 0, VF_NONE, 0, 1) VF_RC(1, 6, 0, 0, 0, VF_NONE, 0, 1)
       VF_RC(1, 4, 0, 0, 0, VF_NONE, 0, 1) VF_RC(1, 4, 0, 0, 1, VF_NONE, 0, 1)  // tests
+      // multi-level Raw / DF chains of the sweeps: Table 2 rows 1-3, 5 (cfg4), 21-25, 34-36 (t512),
+      // cfg5 R(4^3)^3, cfg1 R(3^3)^2
+      VF_RC(2, 4, 3, 0, 0, VF_SVDAG, 4, 5) VF_RC(2, 4, 3, 0, 3, VF_SVDAG, 4, 5) VF_RC(2, 4, 3, 0, 1, VF_SVDAG, 4, 5)
+      VF_RC(3, 4, 4, 3, 0, VF_NONE, 0, 1)
+      VF_RC(2, 3, 3, 0, 3, VF_SVDAG, 3, 5) VF_RC(2, 3, 3, 0, 1, VF_SVDAG, 3, 5) VF_RC(2, 3, 3, 0, 0, VF_SVDAG, 3, 5)
+      VF_RC(3, 3, 3, 3, 0, VF_NONE, 0, 1) VF_RC(3, 4, 1, 4, 0, VF_NONE, 0, 1)
+      VF_RC(2, 5, 4, 0, 3, VF_NONE, 0, 1) VF_RC(2, 5, 4, 0, 1, VF_NONE, 0, 1) VF_RC(2, 5, 4, 0, 0, VF_NONE, 0, 1)
+      VF_RC(3, 4, 4, 4, 0, VF_NONE, 0, 1) VF_RC(2, 3, 3, 0, 0, VF_NONE, 0, 1)
 #undef VF_RC
       default: break;
     }
@@ -1529,6 +1613,8 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
   }
   return VF_OK;
 }
+
+bool has_compiled_in_kernel(const Format& f) { return select_spec(f, false, 0) != nullptr; }
 
 vf_status read_exact_calls(unsigned long long* out, bool reset) {
   VF_CUDA_TRY(cudaMemcpyFromSymbol(out, g_exact_calls, sizeof(*out)));

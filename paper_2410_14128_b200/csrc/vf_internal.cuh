@@ -162,6 +162,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
 vf_status launch_touch_count(const uint32_t* touch, uint64_t n_bitmap_words, unsigned long long* counters,
                              cudaStream_t s);
 vf_status read_exact_calls(unsigned long long* out, bool reset);
+bool has_compiled_in_kernel(const Format& f);
 vf_status launch_query(const Handle* h, const uint32_t* xyz, uint64_t n, uint32_t* out, cudaStream_t s);
 
 #define VF_CUDA_TRY(expr)                                                                   \

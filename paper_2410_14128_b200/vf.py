@@ -60,7 +60,8 @@ class Stats(ctypes.Structure):
                 ("nonempty_voxels", ctypes.c_uint64), ("dims", ctypes.c_uint32 * 3), ("n_levels", ctypes.c_uint32),
                 ("n_tiers", ctypes.c_uint32), ("root", ctypes.c_uint32),
                 ("nodes_per_tier", ctypes.c_uint64 * VF_MAX_TIERS), ("words_per_tier", ctypes.c_uint64 * VF_MAX_TIERS),
-                ("dedup_leaf_nodes", ctypes.c_uint64), ("build_ms", ctypes.c_double)]
+                ("dedup_leaf_nodes", ctypes.c_uint64), ("build_ms", ctypes.c_double), ("compiled_in", ctypes.c_uint32),
+                ("reserved_", ctypes.c_uint32)]
 
 
 _vp = ctypes.c_void_p
@@ -286,7 +287,7 @@ class Handle:
                     nonempty_voxels=s.nonempty_voxels, dims=tuple(s.dims), n_levels=s.n_levels, n_tiers=nt,
                     root=s.root, nodes_per_tier=list(s.nodes_per_tier[:nt]),
                     words_per_tier=list(s.words_per_tier[:nt]), dedup_leaf_nodes=s.dedup_leaf_nodes,
-                    build_ms=s.build_ms)
+                    build_ms=s.build_ms, compiled_in=bool(s.compiled_in))
 
     def buffer(self):
         """(device pointer, n_words) of the format buffer."""

@@ -86,3 +86,24 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(vf.EXPORTED), declared ^ set(vf.EXPORTED)
     for name in declared:
         assert hasattr(vf._lib, name)
+
+
+@pytest.mark.gpu
+def test_every_sweep_format_is_compiled_in():
+    """Every format of the bench sweeps (cfg1-cfg5, cfg4i, t512 = PAPER.md Table 2 rows 1-40) runs a
+    kernel with the format compiled in (the paper's per-format generated code, §4, as a
+    template instance), not the generic tier-table kernel (vf_stats.compiled_in)."""
+    import bench
+    import torch
+    from paper_2410_14128_b200 import vf
+    keys = torch.tensor([1 | (2 << 21) | (3 << 42)], dtype=torch.int64, device="cuda")
+    rgba = torch.tensor([0x01020304], dtype=torch.int32, device="cuda")
+    missing = []
+    for cfg, fmts in bench.SWEEP.items():
+        for fmt in fmts:
+            R = vf.format_resolution(vf.parse_format(fmt))
+            h = vf.build((keys, rgba, tuple(R)), fmt)
+            if not h.stats()["compiled_in"]:
+                missing.append(f"{cfg}: {h.signature}")
+            h.close()
+    assert not missing, missing
