@@ -135,8 +135,14 @@ enum {
   VF_BUILD_WHOLE_LEVEL_DEDUP = 1u << 0, /* one SVDAG de-dup map per level across sub-volumes
                                            (§4.3; evaluated ON).
                                            Clear it for per-sub-volume maps (ablation). */
+  VF_BUILD_ALIGN_NODES = 1u << 1,      /* SVDAG internal nodes ("1 to 9 integers",
+                                           :162) start at 16-B boundaries and are padded to 16-B
+                                           multiples: a node's mask and its first three child
+                                           pointers arrive in one aligned LDG.128 (SURVEY §8(a) a6
+                                           option ii). Costs bytes (vf_stats.bytes_used vs
+                                           paper_layout_bytes); 1-word leaf nodes stay packed. */
   VF_BUILD_DEFAULT = VF_BUILD_WHOLE_LEVEL_DEDUP,
-  VF_BUILD_KNOWN_FLAGS = VF_BUILD_WHOLE_LEVEL_DEDUP /* any other bit: VF_ERR_INVALID_ARG */
+  VF_BUILD_KNOWN_FLAGS = VF_BUILD_WHOLE_LEVEL_DEDUP | VF_BUILD_ALIGN_NODES /* other bits: VF_ERR_INVALID_ARG */
 };
 
 /* Build the format buffer on `device` (stream-ordered on cuda_stream, synchronous before

@@ -375,8 +375,11 @@ __global__ void k_run_flags(const uint64_t* h, uint64_t m, uint64_t* rs) {
   GRID_STRIDE(p, m) { rs[p] = (p == 0 || h[p] != h[p - 1]) ? p : 0; }
 }
 
+// uniq_words: words the record occupies if it is its run's representative, padded to a multiple
+// of `pad` (VF_BUILD_ALIGN_NODES: 4 words = 16 B); uniq_len: the same without padding
 __global__ void k_rep(const uint32_t* words, const uint8_t* len, const uint64_t* svid, const uint32_t* sidx,
-                      const uint64_t* rs, uint64_t m, uint32_t* rep, uint32_t* uniq_words) {
+                      const uint64_t* rs, uint64_t m, uint32_t pad, uint32_t* rep, uint32_t* uniq_words,
+                      uint32_t* uniq_len) {
   GRID_STRIDE(p, m) {
     const uint32_t me = sidx[p];
     uint64_t q = rs[p];
@@ -391,7 +394,8 @@ __global__ void k_rep(const uint32_t* words, const uint8_t* len, const uint64_t*
         }
     }
     rep[me] = r;
-    uniq_words[me] = (r == me) ? len[me] : 0u;
+    uniq_words[me] = (r == me) ? (len[me] + pad - 1) / pad * pad : 0u;
+    uniq_len[me] = (r == me) ? len[me] : 0u;
   }
 }
 
@@ -407,9 +411,11 @@ __global__ void k_rec_write(const uint32_t* words, const uint8_t* len, const uin
 
 // Hash-cons m records. Unique records are laid out in record order (first occurrence, i.e.
 // Morton order of the sub-volume that first needs them) starting at arr_off within `arr`
-// (whose global word offset is base). Returns words written; ptr[i] = global pointer.
+// (whose global word offset is base). Returns words written (each record padded to a multiple of
+// `pad` words); *paper_words = the same without padding; ptr[i] = global pointer.
 uint64_t dedup(Records& R, uint64_t m, dvec<uint32_t>& arr, uint64_t arr_off, uint64_t base,
-               dvec<uint32_t>& ptr, uint64_t* n_unique, cudaStream_t s) {
+               dvec<uint32_t>& ptr, uint64_t* n_unique, cudaStream_t s, uint32_t pad = 1,
+               uint64_t* paper_words = nullptr) {
   auto pol = policy(s);
   dvec<uint64_t> h(m);
   dvec<uint32_t> sidx(m);
@@ -418,9 +424,9 @@ uint64_t dedup(Records& R, uint64_t m, dvec<uint32_t>& arr, uint64_t arr_off, ui
   dvec<uint64_t> rs(m);
   k_run_flags<<<grid_for(m), kThreads, 0, s>>>(raw(h), m, raw(rs));
   thrust::inclusive_scan(pol, rs.begin(), rs.end(), rs.begin(), thrust::maximum<uint64_t>());
-  dvec<uint32_t> rep(m), uw(m);
-  k_rep<<<grid_for(m), kThreads, 0, s>>>(raw(R.words), raw(R.len), raw(R.svid), raw(sidx), raw(rs), m, raw(rep),
-                                          raw(uw));
+  dvec<uint32_t> rep(m), uw(m), ul(m);
+  k_rep<<<grid_for(m), kThreads, 0, s>>>(raw(R.words), raw(R.len), raw(R.svid), raw(sidx), raw(rs), m, pad, raw(rep),
+                                          raw(uw), raw(ul));
   dvec<uint64_t> off(m);
   thrust::transform_exclusive_scan(
       pol, uw.begin(), uw.end(), off.begin(), [] __device__(uint32_t v) { return (uint64_t)v; }, (uint64_t)arr_off,
@@ -437,6 +443,10 @@ uint64_t dedup(Records& R, uint64_t m, dvec<uint32_t>& arr, uint64_t arr_off, ui
   k_rec_write<<<grid_for(m), kThreads, 0, s>>>(raw(R.words), raw(R.len), raw(rep), raw(off), m, base, raw(arr),
                                                 raw(ptr));
   *n_unique = thrust::count_if(pol, uw.begin(), uw.end(), [] __device__(uint32_t v) { return v != 0; });
+  if (paper_words)
+    *paper_words = thrust::transform_reduce(
+        pol, ul.begin(), ul.end(), [] __device__(uint32_t v) -> uint64_t { return (uint64_t)v; }, (uint64_t)0,
+        thrust::plus<uint64_t>());
   return total;
 }
 
@@ -483,6 +493,7 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
   } scope(&h->alloc, s);
   auto pol = policy(s);
   const bool whole = (flags & VF_BUILD_WHOLE_LEVEL_DEDUP) != 0;
+  const bool align = (flags & VF_BUILD_ALIGN_NODES) != 0;
   const uint32_t Rx = f.dims[0], Ry = f.dims[1], Rz = f.dims[2];
 
   try {
@@ -630,10 +641,15 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
                                                         raw(node_start), raw(node_key), M, n, is_root, T.last, whole,
                                                         T.depth, raw(Nn.words), raw(Nn.len), raw(Nn.svid));
         dvec<uint32_t> ptr;
-        uint64_t nu = 0;
-        uint64_t w2 = dedup(Nn, M, arr, off, base, ptr, &nu, s);
+        uint64_t nu = 0, pw2 = 0;
+        // VF_BUILD_ALIGN_NODES: internal nodes start at 16-B boundaries and are padded to 16-B
+        // multiples, so a node's header and its first three child pointers are one aligned LDG.128
+        // (1-word leaf nodes stay packed); the paper's layout counts the unpadded words
+        const uint64_t ioff = align ? (off + 3) & ~3ull : off;
+        uint64_t w2 = dedup(Nn, M, arr, ioff, base, ptr, &nu, s, align ? 4u : 1u, &pw2);
         nodes = nu;
-        words = pwords = off + w2;
+        words = ioff + w2;
+        pwords = off + pw2;
         if (!offsets_fit(t, base, words)) return VF_ERR_OVERFLOW;
         k_ptr_refs<<<grid_for(M), kThreads, 0, s>>>(raw(ptr), M, raw(nr));
       }

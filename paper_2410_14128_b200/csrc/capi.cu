@@ -82,6 +82,7 @@ vf_status vf_build(const vf_volume* vol, const vf_level* levels, uint32_t n_leve
   h->device = device;
   if (alloc) h->alloc.a = *alloc;
   h->build_stream = (cudaStream_t)cuda_stream;
+  h->aligned_nodes = (build_flags & VF_BUILD_ALIGN_NODES) != 0;
   h->fmt = f;
   memset(&h->stats, 0, sizeof(h->stats));
   st = build_format(vol, f, build_flags, (cudaStream_t)cuda_stream, h);

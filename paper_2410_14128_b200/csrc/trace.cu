@@ -227,11 +227,19 @@ __device__ __forceinline__ uint32_t twf(uint32_t w, uint32_t pos, uint32_t len) 
 
 // Node header registers for the current tier. The occupancy mask is 64-bit only when an N^3-tree
 // tier is present (SVO / SVDAG masks are 8-bit: one POPC instead of two on the hot path).
-template <uint32_t KINDS>
-struct Header {
+// ALN (buffers built with VF_BUILD_ALIGN_NODES): an SVDAG node's header load is one aligned
+// LDG.128 that also brings its first three child pointers (kept in base, p1, p2).
+template <bool ALN>
+struct HeaderPtrs {};
+template <>
+struct HeaderPtrs<true> {
+  uint32_t p1, p2;
+};
+template <uint32_t KINDS, bool ALN = false>
+struct Header : HeaderPtrs<ALN> {
   using Mask = typename std::conditional<((KINDS >> K_NTREE) & 1u) != 0, uint64_t, uint32_t>::type;
   Mask mask;      // SVO/SVDAG: valid bits; N^3: 64-bit occupancy
-  uint32_t base;  // SVO: first child; N^3: children block (SVDAG: the node address is N)
+  uint32_t base;  // SVO: first child; N^3: children block; SVDAG + ALN: child pointer 0
   __device__ __forceinline__ uint32_t rank(uint32_t lin) const {
     if constexpr (sizeof(Mask) == 8)
       return __popcll(mask & ((1ull << lin) - 1ull));
@@ -277,9 +285,9 @@ struct Ctr {
 };
 
 // Read the header of node N of a tier of the given kind into h (a Raw tier has none).
-template <uint32_t KINDS, bool COUNT>
+template <uint32_t KINDS, bool COUNT, bool ALN>
 __device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, uint32_t kind, uint32_t N,
-                                            Header<KINDS>& h, Ctr<COUNT>& ct) {
+                                            Header<KINDS, ALN>& h, Ctr<COUNT>& ct) {
   if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
     const uint2 v = __ldg(reinterpret_cast<const uint2*>(buf + N));
     h.base = v.x;
@@ -288,7 +296,15 @@ __device__ __forceinline__ void load_header(const uint32_t* __restrict__ buf, ui
     ct.add(VF_CTR_FORMAT_BYTES, 8);
     ct.touch(N, 2);
   } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-    h.mask = __ldg(buf + N);  // valid bits 0-7 (leaf bits 8-15 never indexed)
+    if constexpr (ALN) {  // 16-B aligned node: mask + child pointers 0..2 in one vector load
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(buf + N));
+      h.mask = v.x;
+      h.base = v.y;
+      h.p1 = v.z;
+      h.p2 = v.w;
+    } else {
+      h.mask = __ldg(buf + N);  // valid bits 0-7 (leaf bits 8-15 never indexed)
+    }
     ct.add(VF_CTR_SVDAG_NODES);
     ct.add(VF_CTR_FORMAT_BYTES, 4);
     ct.touch(N, 1);
@@ -492,7 +508,7 @@ enum { IT_CONTINUE = 0, IT_HIT = 1, IT_MISS = 2 };
 //
 // D (a format descriptor above) compiles the format in: with D::kStatic the tier geometry and
 // flags are functions of the tier index (no tier table, fewer live registers).
-template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec, bool STAGE = false>
+template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec, bool STAGE = false, bool ALN = false>
 struct Lane {
   static constexpr bool SPEC = D::kStatic;
   const uint32_t* s_top;  // STAGE: the top Raw grid (tier 0's node, D::kTopWords words) in shared memory
@@ -546,7 +562,7 @@ struct Lane {
     else return (int)field4(((uint64_t)p.level_top_pack_hi << 32) | p.level_top_pack_lo, tu);
   }
 
-  Header<KINDS> hd;
+  Header<KINDS, ALN> hd;
   int stale;          // axes whose bits below stale_lc are not exact at E
   uint32_t stale_lc;  // bits of V below this are stale on the axes in `stale`
   int moving;         // axes with d != 0
@@ -700,7 +716,7 @@ struct Lane {
     N = p.root;
     hd.mask = 0;
     hd.base = 0;
-    load_header<KINDS>(buf, kind(), N, hd, ct);
+    load_header<KINDS, COUNT, ALN>(buf, kind(), N, hd, ct);
     stale = 0;
     stale_lc = 0;
     return true;
@@ -755,7 +771,10 @@ struct Lane {
         if (has_kind<KINDS>(K_SVO) && kind == K_SVO) {
           child = hd.base + 2u * rank;
         } else if (has_kind<KINDS>(K_SVDAG) && kind == K_SVDAG) {
-          child = __ldg(buf + N + 1u + rank);
+          if constexpr (ALN)
+            child = rank == 0 ? hd.base : rank == 1 ? hd.p1 : rank == 2 ? hd.p2 : __ldg(buf + N + 1u + rank);
+          else
+            child = __ldg(buf + N + 1u + rank);
           ct.add(VF_CTR_SVDAG_PTRS);
           ct.add(VF_CTR_FORMAT_BYTES, 4);
           ct.touch(N + 1u + rank, 1);
@@ -778,7 +797,7 @@ struct Lane {
                                         int nt, uint32_t nN) {
     set_tier(s_tw, nt);
     N = nN;
-    load_header<KINDS>(buf, this->kind(), N, hd, ct);
+    load_header<KINDS, COUNT, ALN>(buf, this->kind(), N, hd, ct);
     // after a descent, the new tier's cell needs V's bits >= lc(); if some of those are stale (the
     // ray moved inside a cell of size 2^stale_lc since they were exact), derive the exact finest
     // voxel of the stale axes within the parent cell (edge 2^lc(t-1); bits above it exact).
@@ -1016,7 +1035,7 @@ __device__ __forceinline__ void stage_tiers(const TraceParams& p, uint32_t* s_tw
 #define VF_TRACE_THREADS 128  // block size (A/B: 256 with VF_MINB 4 keeps the 64-register cap)
 #endif
 constexpr unsigned kTraceThreads = VF_TRACE_THREADS;
-template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec>
+template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec, bool ALN = false>
 __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
                                                     uint64_t n, unsigned long long* __restrict__ counters,
@@ -1027,7 +1046,7 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(con
   Ctr<COUNT> ct;
   ct.touch_map = p.touch;
   if (gid < n) {
-    Lane<KINDS, RESTART, COUNT, D> L;
+    Lane<KINDS, RESTART, COUNT, D, false, ALN> L;
     uint32_t stk[VF_MAX_TIERS];
     int4 out = miss_record();
     if (L.start(p, buf, s_tw, __ldg(rays + 2 * gid), __ldg(rays + 2 * gid + 1), ct)) {
@@ -1324,8 +1343,13 @@ KernelFn select_kernel(uint32_t kinds, bool restart, bool count, bool persistent
 // Compiled-in formats: R(A^3) G(M) (RawSvdag: the cfg4 / cfg5 / t512 headline formats and their
 // sweep neighbours) and the cfg2 / cfg3 headline formats (SparseRaw). Others run the generic kernel.
 // mode 0: one thread per ray; 1: chunked persistent warps; 2: chunked + top Raw grid in shared memory
-template <uint32_t KINDS, class D>
-KernelFn spec_kernel(bool restart, int mode) {
+// ALNOK: the format also gets the VF_BUILD_ALIGN_NODES instance (aligned SVDAG header loads)
+template <uint32_t KINDS, class D, bool ALNOK = false>
+KernelFn spec_kernel(bool restart, int mode, bool aln = false) {
+  if constexpr (ALNOK) {
+    if (aln && mode == 0) return restart ? trace_kernel<KINDS, true, false, D, true> : trace_kernel<KINDS, false, false, D, true>;
+  }
+  (void)aln;
 #ifdef VF_CHUNKED_KERNELS
   if constexpr (D::kTopWords != 0) {
     if (mode == 2) return restart ? trace_chunked<KINDS, true, D, true> : trace_chunked<KINDS, false, D, true>;
@@ -1366,7 +1390,7 @@ bool same_format(const Format& f, const LevelSpec (&lv)[NL]) {
   return true;
 }
 
-KernelFn select_spec(const Format& f, bool restart, int mode) {
+KernelFn select_spec(const Format& f, bool restart, int mode, bool aln) {
 #ifdef VF_ONLY_KINDS
   constexpr uint32_t K = VF_ONLY_KINDS;
 #define VF_HAS(k) (K == (k))
@@ -1378,10 +1402,13 @@ KernelFn select_spec(const Format& f, bool restart, int mode) {
     if (e[0] == e[1] && e[1] == e[2]) switch (((uint32_t)e[0] << 8) | f.levels[1].depth) {
 #define VF_SPEC(a, m) \
   case ((a) << 8) | (m): return spec_kernel<5, RawSvdag<a, m>>(restart, mode);
-        VF_SPEC(4, 7) VF_SPEC(4, 8) VF_SPEC(3, 8) VF_SPEC(3, 7) VF_SPEC(4, 5) VF_SPEC(2, 7) VF_SPEC(6, 5)
-        VF_SPEC(8, 3) VF_SPEC(3, 5) VF_SPEC(3, 9) VF_SPEC(7, 2)
-        VF_SPEC(2, 3) VF_SPEC(1, 4)  // small instances for the parity tests
+#define VF_SPECA(a, m) /* + the VF_BUILD_ALIGN_NODES instance */ \
+  case ((a) << 8) | (m): return spec_kernel<5, RawSvdag<a, m>, true>(restart, mode, aln);
+        VF_SPECA(4, 7) VF_SPECA(4, 8) VF_SPECA(3, 8) VF_SPEC(3, 7) VF_SPEC(4, 5) VF_SPEC(2, 7) VF_SPEC(6, 5)
+        VF_SPEC(8, 3) VF_SPEC(3, 5) VF_SPECA(3, 9) VF_SPEC(7, 2)
+        VF_SPECA(2, 3) VF_SPEC(1, 4)  // small instances for the parity tests
 #undef VF_SPEC
+#undef VF_SPECA
         default: break;
       }
   }
@@ -1407,9 +1434,14 @@ KernelFn select_spec(const Format& f, bool restart, int mode) {
       VF_DS(4, VF_SVDAG, 7) VF_DS(6, VF_SVDAG, 5) VF_DS(4, VF_SVO, 7) VF_DS(6, VF_SVO, 5) VF_DS(4, VF_SVDAG, 5)
       VF_DS(4, VF_SVO, 5) VF_DS(2, VF_SVDAG, 2)
 #undef VF_DS
-      VF_TS(0, VF_SVDAG, 1, 11, 4) VF_TS(0, VF_SVO, 1, 11, 2) VF_TS(0, VF_SVDAG, 1, 8, 4) VF_TS(0, VF_SVO, 1, 8, 2)
-      VF_TS(0, VF_SVDAG, 1, 10, 4) VF_TS(0, VF_SVO, 1, 10, 2) VF_TS(0, VF_SVDAG, 1, 12, 4) VF_TS(0, VF_SVO, 1, 12, 2)
+#define VF_TSA(a, k, lf, ns, kinds) /* + the VF_BUILD_ALIGN_NODES instance */ \
+  case ((a) << 24) | ((k) << 16) | ((lf) << 8) | (ns): \
+    return spec_kernel<kinds, TopSparse<a, K_OF_##k, lf, ns>, true>(restart, mode, aln);
+      VF_TSA(0, VF_SVDAG, 1, 11, 4) VF_TS(0, VF_SVO, 1, 11, 2) VF_TSA(0, VF_SVDAG, 1, 8, 4) VF_TS(0, VF_SVO, 1, 8, 2)
+      VF_TS(0, VF_SVDAG, 1, 10, 4) VF_TS(0, VF_SVO, 1, 10, 2) VF_TSA(0, VF_SVDAG, 1, 12, 4) VF_TS(0, VF_SVO, 1, 12, 2)
+#undef VF_TSA
       VF_TS(0, VF_SVDAG, 1, 9, 4) VF_TS(0, VF_SVO, 1, 9, 2)
+      VF_TS(0, VF_SVDAG, 1, 6, 4) VF_TS(0, VF_SVO, 1, 6, 2) VF_TS(0, VF_NTREE, 2, 3, 8)  // cfg1 sweep
       VF_TS(4, VF_SVO, 1, 7, 3) VF_TS(6, VF_SVO, 1, 5, 3) VF_TS(4, VF_SVO, 1, 5, 3)
       VF_TS(0, VF_NTREE, 2, 4, 8) VF_TS(0, VF_NTREE, 2, 5, 8) VF_TS(0, VF_NTREE, 2, 6, 8) VF_TS(1, VF_NTREE, 2, 5, 9)
       VF_TS(4, VF_NTREE, 2, 4, 9)
@@ -1545,7 +1577,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
   if (chunked_env >= 0) mode = chunked_env;
   bool chunked = false;
   if (!persistent && !counters && !no_spec)
-    if (KernelFn sf = select_spec(h->fmt, (flags & VF_TRACE_RESTART_SV) != 0, mode)) {
+    if (KernelFn sf = select_spec(h->fmt, (flags & VF_TRACE_RESTART_SV) != 0, mode, h->aligned_nodes)) {
       fn = sf;
       chunked = mode > 0;
     }
@@ -1614,7 +1646,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
   return VF_OK;
 }
 
-bool has_compiled_in_kernel(const Format& f) { return select_spec(f, false, 0) != nullptr; }
+bool has_compiled_in_kernel(const Format& f) { return select_spec(f, false, 0, false) != nullptr; }
 
 vf_status read_exact_calls(unsigned long long* out, bool reset) {
   VF_CUDA_TRY(cudaMemcpyFromSymbol(out, g_exact_calls, sizeof(*out)));

@@ -121,6 +121,7 @@ struct Handle {
   uint32_t* buf = nullptr;  // device words
   uint64_t n_words = 0;
   size_t buf_bytes = 0;     // allocated bytes of buf (n_words + guard words)
+  bool aligned_nodes = false;  // built with VF_BUILD_ALIGN_NODES (16-B aligned SVDAG nodes)
   vf_stats stats{};
   // staging and pipeline streams for vf_trace_host
   void* stage = nullptr;

@@ -27,6 +27,7 @@ STATUS_NAMES = {0: "VF_OK", 1: "VF_ERR_INVALID_ARG", 2: "VF_ERR_PARSE", 3: "VF_E
 VF_RAW, VF_SVO, VF_SVDAG, VF_NTREE, VF_DF = range(5)
 VF_VOL_DENSE_DEVICE, VF_VOL_SPARSE_DEVICE = 0, 1
 VF_BUILD_WHOLE_LEVEL_DEDUP = 1
+VF_BUILD_ALIGN_NODES = 2
 VF_BUILD_DEFAULT = VF_BUILD_WHOLE_LEVEL_DEDUP
 VF_TRACE_RESTART_SV = 1
 VF_TRACE_INCOHERENT = 2

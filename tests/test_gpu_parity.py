@@ -418,3 +418,40 @@ def test_nonfinite_rays_miss():
     xyz, t = gpu_trace(h, rays)
     assert (xyz[:7] == -1).all() and np.isinf(t[:7]).all()
     assert tuple(xyz[7]) == (1, 1, 0)  # the unmodified ray hits
+
+
+# ---------------------------------------------------------------- VF_BUILD_ALIGN_NODES (a6 option ii)
+@pytest.mark.parametrize("fmt,R_", [("R(2^3) G(3)", 32), ("R(4^3) G(7)", 2048)])
+def test_align_nodes_parity_and_bytes(fmt, R_):
+    """SVDAG nodes padded to 16-B multiples: the
+    same first hits as the oracle (stack and restart, through the aligned-header kernel), the same
+    paper-layout bytes as the packed build, more device bytes, and every internal node 16-B
+    aligned (its child pointers, read back from the buffer, are multiples of 4 words)."""
+    import torch
+    vf = _vf()
+    if R_ == 32:
+        d = inputs.random_occupancy((32,) * 3, 0.05, 0xA11)
+        rays = _rays_small((32,) * 3, 61)
+    else:
+        d = inputs.city(2048)
+        rays = R.camera("city", scale=4)[0]
+    keys, rgba = inputs.voxels_device(d)
+    hp = vf.build((keys, rgba, inputs.dims_of(d)), fmt)
+    ha = vf.build((keys, rgba, inputs.dims_of(d)), fmt, flags=vf.VF_BUILD_DEFAULT | vf.VF_BUILD_ALIGN_NODES)
+    sp, sa = hp.stats(), ha.stats()
+    assert sa["paper_layout_bytes"] == sp["paper_layout_bytes"] and sa["bytes_used"] > sp["bytes_used"]
+    assert sa["compiled_in"]
+    # the top Raw grid's non-zero cells are SVDAG root pointers: all 16-B aligned
+    top = ha.buffer_words(sa["root"], 8 ** int(fmt[2]) if R_ == 32 else 16 ** 3)
+    assert top.any() and (top[top != 0] % 4 == 0).all()
+    g = oracle.Grid.from_generator(d)
+    ref = g.trace(rays)
+    for restart in (False, True):
+        xyz, t = gpu_trace(ha, rays, restart)
+        assert_parity(xyz, t, ref, f"{fmt} aligned restart={restart}")
+        xp, tp = gpu_trace(hp, rays, restart)
+        assert np.array_equal(xyz, xp) and np.array_equal(t.view(np.int32), tp.view(np.int32))
+    hp.close()
+    ha.close()
+    del keys, rgba
+    torch.cuda.empty_cache()

@@ -16,7 +16,9 @@ pers = sys.argv[2] == "1"
 vname, _, deffmt, _ = bench.CONFIGS[cfg]
 vol = bench.make_volume(vname)
 k, c = inputs.voxels_device(vol)
-h = vf.build((k, c, inputs.dims_of(vol)), fmt or deffmt)
+fl = vf.VF_BUILD_DEFAULT | (vf.VF_BUILD_ALIGN_NODES if os.environ.get("VF_AB_ALIGN") else 0)
+h = vf.build((k, c, inputs.dims_of(vol)), fmt or deffmt, flags=fl)
+mib = h.stats()["bytes_used"] / 2**20
 del k, c
 rays = torch.from_numpy(bench.make_rays(cfg)[0]).cuda()
 hits = torch.empty((rays.shape[0], 4), dtype=torch.int32, device="cuda")
@@ -31,7 +33,7 @@ for restart in (False, True):
         a.record(); h.trace(rays, hits, restart=restart, persistent=pers); b.record()
         torch.cuda.synchronize(); ms.append(a.elapsed_time(b))
     res.append(rays.shape[0] / statistics.median(ms) / 1e3)
-print(f"stack {res[0]:.0f} restart {res[1]:.0f}")
+print(f"stack {res[0]:.0f} restart {res[1]:.0f} ({mib:.1f} MiB)")
 '''
 spec = sys.argv[1]
 modes = sys.argv[2:]
