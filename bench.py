@@ -5,10 +5,12 @@ Default workload: cfg5 of BASELINE.json (`configs[4]`, the config the metric's "
 quoted on) — the 4096^3 sparse procedural volume (inputs.sparse, seed 0x4096), one 3840x2160
 perspective frame, format R(4^3) G(8) (the best hybrid of the cfg5 sweep, profiles/). A step = ONE
 FRAME: its rays are sharded over the N GPUs by interleaved 16x16 screen tiles (tile mod N; the
-volume is replicated on every GPU), every rank traces its tiles with vf_trace (all §8(a) rows run
-inside the one trace kernel) and the hit records are gathered to rank 0 with NCCL — the one
-collective (north_star); at N = 1 the frame is one trace launch. Total work is
-fixed as N grows ("scaling": "strong"). Inputs are resident in HBM; L2 (126 MB) is flushed between
+volume is replicated on every GPU), every rank traces its tiles (all §8(a) rows run inside the one
+trace kernel) and the hits reach rank 0's frame buffer through the one collective (north_star,
+SURVEY.md §8(e)): by default fused into the trace kernel itself — vf_trace_scatter stores each hit
+at its pixel in rank 0's frame over NVLink (CUDA IPC), then a one-int all-reduce signals completion
+(--gather p2p); or a chunked trace + NCCL gather pipeline (--gather nccl, also the fallback). At
+N = 1 the frame is one trace launch. Total work is fixed as N grows ("scaling": "strong"). Inputs are resident in HBM; L2 (126 MB) is flushed between
 timed steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -247,43 +249,73 @@ def max_over_ranks(vals, dev, dist_on):
 
 
 class FrameStep:
-    """One frame on N ranks: this rank's interleaved 16x16 tiles are traced in
-    K chunks; after chunk k is traced its hit records are gathered to rank 0 asynchronously over
-    NCCL, so the transfer overlaps the trace of chunk k+1 (shard.ChunkedGather). With one rank
-    (and no --force-dist) the frame is one trace launch and there is nothing to gather.
-    `trace(rays_view, hits_view)` launches one trace on the current stream."""
+    """One frame on N ranks. Two forms of the one collective:
+    * "p2p" (default for N > 1): the fused trace + gather — every rank's trace kernel stores its
+      interleaved 16x16 tiles' hits straight into rank 0's frame buffer over NVLink / NVSwitch
+      (vf_trace_scatter into a CUDA-IPC-mapped peer buffer, shard.PeerFrame), then a one-int
+      all-reduce signals completion;
+    * "nccl": this rank's tiles are traced in K chunks; after chunk k is traced its hit records are
+      gathered to rank 0 asynchronously over NCCL, so the transfer overlaps the trace of chunk k+1
+      (shard.ChunkedGather). Also the fallback when the peer mapping fails.
+    With one rank (and no --force-dist) the frame is one trace launch and there is nothing to
+    gather. `trace(rays_view, hits_view)` / `trace_scatter(rays, dest_ptr, slots)` launch one trace
+    on the current stream."""
 
-    def __init__(self, trace, rays_local, counts, rank, world, dist_on, device, chunks=0, timed=True):
+    def __init__(self, trace, rays_local, counts, rank, world, dist_on, device, chunks=0, timed=True,
+                 trace_scatter=None, pixels_local=None, n_total=0, gather="p2p"):
         import torch
         from paper_2410_14128_b200 import shard
         self.trace, self.rays, self.timed = trace, rays_local, timed
+        self.trace_scatter = trace_scatter
         self.n_local = counts[rank]
-        self.pipe = None
-        if dist_on:
+        self.pipe = self.peer = None
+        self.gather = "none"
+        self.gather_note = ""
+        if dist_on and gather == "p2p" and trace_scatter is not None:
+            try:
+                self.peer = shard.PeerFrame(n_total, pixels_local, device)
+                self.gather = "p2p"
+            except Exception as e:  # every rank raises together (PeerFrame agrees on failure)
+                self.gather_note = f"p2p unavailable ({e}); NCCL gather"
+        if dist_on and self.peer is None:
             k = chunks if chunks > 0 else max(1, min(4, max(counts) // (1 << 19)))
             self.pipe = shard.ChunkedGather(counts, k, device)
             self.hits = self.pipe.hits
+            self.gather = "nccl"
+        elif self.peer is not None:
+            self.hits = None  # the frame lives on rank 0 (pixel order); local_hits() reads it back
         else:
             self.hits = torch.empty((self.n_local, 4), dtype=torch.int32, device=device)
         self.launches = len(self.pipe.bounds) if self.pipe else 1
         self.kernel_events = []
 
-    def _trace(self, lo, hi, hv):
+    def _timed(self, fn, *a):
         import torch
         if self.timed:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            self.trace(self.rays[lo:hi], hv)
-            b.record()
-            self.kernel_events.append((a, b))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(*a)
+            e1.record()
+            self.kernel_events.append((e0, e1))
         else:
-            self.trace(self.rays[lo:hi], hv)
+            fn(*a)
+
+    def _trace(self, lo, hi, hv):
+        self._timed(self.trace, self.rays[lo:hi], hv)
 
     def __call__(self):
+        if self.peer is not None:
+            return self.peer.run(lambda r, ptr, sl: self._timed(self.trace_scatter, r, ptr, sl), self.rays)
         if self.pipe is None:
             self._trace(0, self.n_local, self.hits)
             return None
         return self.pipe.run(self._trace)
+
+    def local_hits(self):
+        """This rank's hits in its own ray order (rank 0 only in p2p mode)."""
+        if self.peer is not None:
+            return self.peer.frame[self.peer.slots.long()] if self.peer.frame is not None else None
+        return self.hits[:self.n_local]
 
     def kernel_ms(self):
         """Sum of the trace launches' CUDA-event durations since the last call (then reset)."""
@@ -410,7 +442,11 @@ def run_ours(args):
     def trace(rv, hv):
         handle.trace(rv, hv, restart=args.restart, incoherent=incoh)
 
-    step = FrameStep(trace, rays, counts, rank, world, dist_on, dev, args.gather_chunks)
+    def trace_scatter(rv, ptr, slots):
+        handle.trace_scatter(rv, ptr, slots, restart=args.restart, incoherent=incoh)
+
+    step = FrameStep(trace, rays, counts, rank, world, dist_on, dev, args.gather_chunks,
+                     trace_scatter=trace_scatter, pixels_local=perm[own], n_total=n_total, gather=args.gather)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -492,7 +528,7 @@ def run_ours(args):
             issue = {"bound": "issue", "frac": round(ach_i / peak_i, 3), "unit": "warp-inst/s",
                      "warp_inst_per_ray": round(ent["warp_inst_per_launch"] / ent_rays, 1),
                      "threads_per_warp_inst": round(ent.get("thread_inst_per_launch", 0) / ent["warp_inst_per_launch"], 1)}
-        hits_np = step.hits[:counts[rank]].cpu().numpy()
+        hits_np = step.local_hits().cpu().numpy()
         gxyz, gt = hits_np[:, :3], hits_np[:, 3].view(np.float32)
         cpu = None
         sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -511,8 +547,11 @@ def run_ours(args):
                        "hit_rate": round(float((gxyz[:, 0] >= 0).mean()), 4), "build_s": round(build_s, 3),
                        "voxel_gen_s": round(gen_s, 2), "l2": "flushed between timed steps (2x126 MB write)",
                        "parallelism": f"tile{world}: one frame's 16x16 tiles interleaved over {world} GPU(s), volume "
-                                      f"replicated" + (f", NCCL gather of hits to rank 0 in {step.launches} chunks"
-                                                       if dist_on else "")},
+                                      f"replicated" + (
+                                          ", fused trace + hit scatter into rank 0's frame over peer memory (CUDA IPC)"
+                                          if step.gather == "p2p" else
+                                          f", NCCL gather of hits to rank 0 in {step.launches} chunks"
+                                          if dist_on else "") + (f" [{step.gather_note}]" if step.gather_note else "")},
             "e2e": {"value": round(e2e_val, 1), "unit": "Mrays/s", "h2d_bytes_per_step": n_total * 32,
                     "d2h_bytes_per_step": n_total * 16},
             "gpu_launches": step.launches * args.steps,
@@ -523,7 +562,8 @@ def run_ours(args):
             result["cfg4_2048"] = side_cfg4(args, stream, flush)
         if args.sweep and world == 1 and cfg in SWEEP:
             out = args.sweep_out or os.path.join(ROOT, "profiles", f"r2_{cfg}_sweep.json")
-            rows = sweep(cfg, vol, rays, step.hits, stream, flush, args)
+            hb = step.hits if step.hits is not None else torch.empty((rays.shape[0], 4), dtype=torch.int32, device=dev)
+            rows = sweep(cfg, vol, rays, hb, stream, flush, args)
             with open(out, "w") as f:
                 json.dump({"config": cfg, "rows": rows, "clocks": clk}, f, indent=1)
             result["sweep_file"] = os.path.relpath(out, ROOT)
@@ -674,7 +714,9 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-side", action="store_true", help="skip the cfg4 2048^3 side measurement")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--gather-chunks", type=int, default=0, help="N>1: trace/gather pipeline depth (0: auto)")
+    ap.add_argument("--gather-chunks", type=int, default=0, help="N>1 nccl gather: trace/gather pipeline depth (0: auto)")
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1: fused trace + peer-memory hit scatter (p2p) or trace + NCCL gather")
     ap.add_argument("--force-dist", action="store_true", help="test aid: the N>1 code path with one rank")
     argv = sys.argv[1:] if argv is None else argv
     args = ap.parse_args(argv)

@@ -210,6 +210,30 @@ typedef struct {
 VF_API vf_status vf_trace_ex(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, vf_payload* payload,
                              uint32_t trace_flags, void* cuda_stream);
 
+/* Fused trace + hit gather (north_star multi-GPU): the hit of ray i is stored at
+ * hits[slots[i]] instead of hits[i]. `slots` is a device array of n u32 on h's device; `hits` is
+ * 16-B aligned and may be ANOTHER GPU's frame buffer mapped into this process by vf_ipc_open (or a
+ * peer pointer with peer access enabled): each rank then writes its screen tiles' hits straight
+ * into rank 0's image over NVLink / NVSwitch from the trace kernel itself, so the gather overlaps
+ * the trace ray by ray and no NCCL gather or host-side un-permutation is needed. The writes are
+ * complete when the stream synchronises (a kernel's stores are performed at its completion);
+ * the consumer learns that from the caller's own signal (e.g. a barrier). Slots must be distinct
+ * within the frame. Same kernels and results as vf_trace. */
+VF_API vf_status vf_trace_scatter(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits,
+                                  const uint32_t* slots, uint32_t trace_flags, void* cuda_stream);
+
+/* CUDA IPC for vf_trace_scatter's destination: vf_ipc_export describes a device allocation of this
+ * process (any pointer inside it; the offset is recorded), vf_ipc_open maps another process's
+ * export on `device` (peer access enabled on demand) and returns the pointer the exporter named;
+ * vf_ipc_close unmaps it. A process cannot open its own export (use the pointer itself). */
+typedef struct {
+  uint8_t handle[64]; /* cudaIpcMemHandle_t of the allocation */
+  uint64_t offset;    /* byte offset of the exported pointer inside that allocation */
+} vf_ipc_handle;
+VF_API vf_status vf_ipc_export(const void* dev_ptr, vf_ipc_handle* out);
+VF_API vf_status vf_ipc_open(const vf_ipc_handle* in, int device, void** dev_ptr);
+VF_API vf_status vf_ipc_close(void* dev_ptr);
+
 /* End-to-end variant with HOST buffers: copies rays host->device, traces, copies hits
  * device->host and returns when the hits are on the host. Large frames are cut into chunks
  * pipelined over the handle's internal streams (copy-in of chunk i+1, trace of chunk i and

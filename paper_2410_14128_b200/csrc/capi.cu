@@ -5,6 +5,8 @@
 
 #include <new>
 
+#include <cuda.h>
+
 #include "vf_internal.cuh"
 
 using namespace vf;
@@ -14,6 +16,22 @@ struct vf_handle : vf::Handle {};
 namespace {
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// Base address of the device allocation containing p (driver cuMemGetAddressRange, fetched through
+// the runtime so that libvf.so does not link libcuda: it must load on machines without a driver).
+bool allocation_base(const void* p, CUdeviceptr* base) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return (Fn)f;
+  }();
+  size_t size = 0;
+  return fn && fn(base, &size, (CUdeviceptr)p) == CUDA_SUCCESS;
+}
 
 struct DeviceGuard {
   int prev = -1;
@@ -147,6 +165,70 @@ vf_status vf_trace_ex(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit
   }
   DeviceGuard g(h->device);
   return launch_trace(h, rays, n, hits, trace_flags, (cudaStream_t)cuda_stream, nullptr, payload);
+}
+
+vf_status vf_trace_scatter(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, const uint32_t* slots,
+                           uint32_t trace_flags, void* cuda_stream) {
+  clear_error();
+  if (!h) {
+    set_error("vf_trace_scatter: null handle");
+    return VF_ERR_INVALID_ARG;
+  }
+  if (n == 0) return VF_OK;
+  if (!rays || !hits || !slots || !aligned16(rays) || !aligned16(hits) || ((uintptr_t)slots & 3u)) {
+    set_error("vf_trace_scatter: rays/hits must be 16-byte aligned device pointers, slots a 4-byte aligned device array");
+    return VF_ERR_INVALID_ARG;
+  }
+  DeviceGuard g(h->device);
+  return launch_trace(h, rays, n, hits, trace_flags, (cudaStream_t)cuda_stream, nullptr, nullptr, nullptr, slots);
+}
+
+vf_status vf_ipc_export(const void* dev_ptr, vf_ipc_handle* out) {
+  clear_error();
+  if (!dev_ptr || !out) {
+    set_error("vf_ipc_export: null argument");
+    return VF_ERR_INVALID_ARG;
+  }
+  memset(out, 0, sizeof(*out));
+  CUdeviceptr base = 0;
+  if (!allocation_base(dev_ptr, &base)) {
+    set_error("vf_ipc_export: %p is not a device allocation", dev_ptr);
+    return VF_ERR_INVALID_ARG;
+  }
+  cudaIpcMemHandle_t hd;
+  VF_CUDA_TRY(cudaIpcGetMemHandle(&hd, (void*)base));
+  static_assert(sizeof(hd) <= sizeof(out->handle), "cudaIpcMemHandle_t size");
+  memcpy(out->handle, &hd, sizeof(hd));
+  out->offset = (uint64_t)((CUdeviceptr)dev_ptr - base);
+  return VF_OK;
+}
+
+vf_status vf_ipc_open(const vf_ipc_handle* in, int device, void** dev_ptr) {
+  clear_error();
+  if (!in || !dev_ptr) {
+    set_error("vf_ipc_open: null argument");
+    return VF_ERR_INVALID_ARG;
+  }
+  *dev_ptr = nullptr;
+  DeviceGuard g(device);
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, in->handle, sizeof(hd));
+  void* base = nullptr;
+  VF_CUDA_TRY(cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr = (char*)base + in->offset;
+  return VF_OK;
+}
+
+vf_status vf_ipc_close(void* dev_ptr) {
+  clear_error();
+  if (!dev_ptr) return VF_OK;
+  CUdeviceptr base = 0;
+  if (!allocation_base(dev_ptr, &base)) {
+    set_error("vf_ipc_close: %p is not a mapped device pointer", dev_ptr);
+    return VF_ERR_INVALID_ARG;
+  }
+  VF_CUDA_TRY(cudaIpcCloseMemHandle((void*)base));
+  return VF_OK;
 }
 
 vf_status vf_trace_counters(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t trace_flags,

@@ -1060,7 +1060,7 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(con
         ct.add(VF_CTR_HITS);
       }
     }
-    hits[gid] = out;
+    hits[p.slot ? __ldg(p.slot + gid) : gid] = out;  // vf_trace_scatter: fused hit gather
 #ifdef VF_RAY_TESTS  // analysis build (tools/ray_tests_dump.py): per-ray cell tests of the counting run
     if (COUNT) hits[gid].x = (int)ct.v[VF_CTR_CELL_TESTS];
 #endif
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(kPersistThreads, VF_PMINB) trace_persistent(co
           if (L.start(p, buf, s_tw, __ldg(rays + 2 * idx), __ldg(rays + 2 * idx + 1), ct))
             active = true;
           else {
-            hits[idx] = miss_record();
+            hits[p.slot ? __ldg(p.slot + idx) : idx] = miss_record();
             if (p.payload) p.payload[idx] = make_uint2(0u, 0u);
           }
         }
@@ -1126,7 +1126,7 @@ __global__ void __launch_bounds__(kPersistThreads, VF_PMINB) trace_persistent(co
       const int res = L.iterate(p, buf, s_tw, stk, ct);
       if (res != IT_CONTINUE) {
         if (res == IT_HIT) ct.add(VF_CTR_HITS);
-        hits[idx] = res == IT_HIT ? L.hit_record() : miss_record();
+        hits[p.slot ? __ldg(p.slot + idx) : idx] = res == IT_HIT ? L.hit_record() : miss_record();
         if (p.payload) p.payload[idx] = res == IT_HIT ? L.payload_record(buf) : make_uint2(0u, 0u);
         active = false;
       }
@@ -1197,7 +1197,7 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks)
         if (L.start(p, buf, s_tw, __ldg(rays + 2 * idx), __ldg(rays + 2 * idx + 1), ct)) {
           active = true;
         } else {
-          hits[idx] = miss_record();
+          hits[p.slot ? __ldg(p.slot + idx) : idx] = miss_record();
           if (p.payload) p.payload[idx] = make_uint2(0u, 0u);
         }
       }
@@ -1216,7 +1216,7 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks)
         if (keep > 0 && (unsigned)__popc(__activemask()) <= keep) break;
       }
       if (res != IT_CONTINUE) {
-        hits[idx] = res == IT_HIT ? L.hit_record() : miss_record();
+        hits[p.slot ? __ldg(p.slot + idx) : idx] = res == IT_HIT ? L.hit_record() : miss_record();
         if (p.payload) p.payload[idx] = res == IT_HIT ? L.payload_record(buf) : make_uint2(0u, 0u);
         active = false;
       }
@@ -1562,7 +1562,7 @@ int persistent_blocks(KernelFn fn, int device, size_t smem = 0) {
 }  // namespace
 
 vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags, cudaStream_t s,
-                       unsigned long long* counters, vf_payload* payload, uint32_t* touch) {
+                       unsigned long long* counters, vf_payload* payload, uint32_t* touch, const uint32_t* slots) {
   if (n == 0) return VF_OK;
   uint32_t kinds = 0;
   for (uint32_t t = 0; t < h->fmt.n_tiers; ++t) kinds |= 1u << h->fmt.tiers[t].kind;
@@ -1599,6 +1599,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     TraceParams tp = h->tp;
     tp.payload = reinterpret_cast<uint2*>(payload);
     tp.touch = touch;
+    tp.slot = slots;
     if (chunk_env) tp.chunk = chunk_env;
     if (crefill_env) tp.crefill = crefill_env;
     const uint32_t slot = h->work_slot.fetch_add(1) % kWorkSlots;
@@ -1615,6 +1616,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     TraceParams tp = h->tp;
     tp.payload = reinterpret_cast<uint2*>(payload);
     tp.touch = touch;
+    tp.slot = slots;
     if (refill_env) tp.refill = (uint32_t)refill_env;
     const uint32_t slot = h->work_slot.fetch_add(1) % kWorkSlots;
     unsigned long long* work = h->work + 2 * slot;
@@ -1635,6 +1637,7 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     TraceParams tp = h->tp;
     tp.payload = reinterpret_cast<uint2*>(payload);
     tp.touch = touch;
+    tp.slot = slots;
     fn<<<(unsigned)blocks, threads, 0, s>>>(tp, h->buf, reinterpret_cast<const float4*>(rays),
                                             reinterpret_cast<int4*>(hits), n, counters, nullptr);
   }

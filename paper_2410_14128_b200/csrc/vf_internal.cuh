@@ -59,6 +59,7 @@ struct TraceParams {
   uint32_t crefill;     // chunked trace: refill from the warp's chunk when >= crefill lanes are idle
   uint32_t df_mask;     // bit t: tier t is a DF grid (2-word cells {TermInt, L1 distance})
   uint2* payload;       // optional closest-hit payload output (vf_trace_ex), per launch
+  const uint32_t* slot; // optional hit destination index per ray (vf_trace_scatter), per launch
   uint32_t* touch;      // counting launches: touch bitmap, one bit per format word (else null)
   uint32_t lf0[3];      // tier-0 fan-out per axis (log2)
   int32_t dims[3];      // resolution per axis
@@ -159,7 +160,7 @@ vf_status build_format(const vf_volume* vol, const Format& f, uint32_t flags, cu
 // trace.cu
 vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags,
                        cudaStream_t s, unsigned long long* counters = nullptr, vf_payload* payload = nullptr,
-                       uint32_t* touch = nullptr);
+                       uint32_t* touch = nullptr, const uint32_t* slots = nullptr);
 vf_status launch_touch_count(const uint32_t* touch, uint64_t n_bitmap_words, unsigned long long* counters,
                              cudaStream_t s);
 vf_status read_exact_calls(unsigned long long* out, bool reset);

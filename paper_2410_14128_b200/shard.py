@@ -1,4 +1,5 @@
-"""Screen-tile sharding of a frame across ranks and the one collective (hit gather).
+"""Screen-tile sharding of a frame across ranks and the one collective (hit gather): NCCL
+(ChunkedGather) or the fused trace + peer-memory scatter (PeerFrame).
 
 north_star / SURVEY.md §8(e): the volume is replicated on every GPU, the frame's rays are
 sharded by screen tiles, and NCCL is used only for the final hit-buffer gather. Tiles are
@@ -91,6 +92,58 @@ class ChunkedGather:
         if self.recv is None:
             return None
         return [b[:c] for b, c in zip(self.recv, self.counts)]
+
+
+class PeerFrame:
+    """The fused trace + gather of one frame over peer memory (the task's "compute
+    step followed by a collective in ONE kernel"): rank 0 owns the frame's hit buffer in
+    row-major pixel order; every rank maps it (CUDA IPC, vf_ipc_open: NVLink / NVSwitch between
+    GPUs of one node) and traces its interleaved tiles with vf_trace_scatter, whose kernel stores
+    each hit straight into rank 0's image at the ray's pixel. A one-int all-reduce after the trace
+    is the completion signal (stream-ordered after every rank's kernel). No hit gather, no
+    un-permutation. Raises on any rank if the mapping fails on any rank (the caller falls back to
+    ChunkedGather)."""
+
+    def __init__(self, n_total: int, pixels_local: np.ndarray, device, group=None):
+        import torch
+        import torch.distributed as dist
+        from paper_2410_14128_b200 import vf
+        self.rank, self.group = dist.get_rank(group), group
+        self.device = device
+        self.frame = torch.empty((n_total, 4), dtype=torch.int32, device=device) if self.rank == 0 else None
+        blob = [vf.ipc_export(self.frame) if self.rank == 0 else None]
+        dist.broadcast_object_list(blob, src=0, group=group)
+        err = ""
+        self.ptr, self._opened = 0, False
+        if self.rank == 0:
+            self.ptr = self.frame.data_ptr()
+        else:
+            try:
+                self.ptr = vf.ipc_open(blob[0], device.index)
+                self._opened = True
+            except Exception as e:  # reported to every rank below
+                err = str(e)
+        errs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(errs, err, group=group)
+        if any(errs):
+            self.close()
+            raise RuntimeError("peer frame mapping failed: " + "; ".join(e for e in errs if e))
+        self.slots = torch.from_numpy(np.ascontiguousarray(pixels_local, dtype=np.int32)).to(device)
+        self.flag = torch.ones(1, dtype=torch.int32, device=device)
+
+    def run(self, trace_scatter, rays):
+        """trace_scatter(rays, dest_ptr, slots) traces this rank's rays into the shared frame; then the
+        completion signal. Returns the frame on rank 0 (row-major pixels), None elsewhere."""
+        import torch.distributed as dist
+        trace_scatter(rays, self.ptr, self.slots)
+        dist.all_reduce(self.flag, group=self.group)
+        return self.frame
+
+    def close(self):
+        from paper_2410_14128_b200 import vf
+        if self._opened:
+            vf.ipc_close(self.ptr)
+            self._opened = False
 
 
 def assemble(bufs, perm: np.ndarray, width: int, world: int, tile: int = TILE) -> np.ndarray:

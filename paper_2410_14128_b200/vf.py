@@ -56,6 +56,29 @@ class Volume(ctypes.Structure):
                 ("n_voxels", ctypes.c_uint64), ("keys", ctypes.c_void_p), ("values", ctypes.c_void_p)]
 
 
+class IpcHandle(ctypes.Structure):  # vf_ipc_handle
+    _fields_ = [("handle", ctypes.c_uint8 * 64), ("offset", ctypes.c_uint64)]
+
+
+def ipc_export(tensor) -> bytes:
+    """vf_ipc_export of a CUDA tensor's data pointer (bytes, for any host-side transport)."""
+    h = IpcHandle()
+    _check(_lib.vf_ipc_export(ctypes.c_void_p(tensor.data_ptr()), ctypes.byref(h)))
+    return bytes(ctypes.string_at(ctypes.addressof(h), ctypes.sizeof(h)))
+
+
+def ipc_open(blob: bytes, device: int) -> int:
+    """vf_ipc_open: map another process's export on `device`; returns the device pointer (int)."""
+    h = IpcHandle.from_buffer_copy(blob)
+    out = ctypes.c_void_p(0)
+    _check(_lib.vf_ipc_open(ctypes.byref(h), device, ctypes.byref(out)))
+    return out.value
+
+
+def ipc_close(ptr: int) -> None:
+    _check(_lib.vf_ipc_close(ctypes.c_void_p(ptr)))
+
+
 class Stats(ctypes.Structure):
     _fields_ = [("bytes_used", ctypes.c_uint64), ("paper_layout_bytes", ctypes.c_uint64),
                 ("nonempty_voxels", ctypes.c_uint64), ("dims", ctypes.c_uint32 * 3), ("n_levels", ctypes.c_uint32),
@@ -103,6 +126,10 @@ _sig = {
                   _vp, ctypes.POINTER(_vp), ctypes.POINTER(_u64)], ctypes.c_int),
     "vf_trace": ([_vp, _vp, _u64, _vp, _u32, _vp], ctypes.c_int),
     "vf_trace_host": ([_vp, _vp, _u64, _vp, _u32, _vp], ctypes.c_int),
+    "vf_trace_scatter": ([_vp, _vp, _u64, _vp, _vp, _u32, _vp], ctypes.c_int),
+    "vf_ipc_export": ([_vp, _vp], ctypes.c_int),
+    "vf_ipc_open": ([_vp, ctypes.c_int, ctypes.POINTER(_vp)], ctypes.c_int),
+    "vf_ipc_close": ([_vp], ctypes.c_int),
     "vf_trace_ex": ([_vp, _vp, _u64, _vp, _vp, _u32, _vp], ctypes.c_int),
     "vf_trace_counters": ([_vp, _vp, _u64, _vp, _u32, _vp, ctypes.POINTER(_u64)], ctypes.c_int),
     "vf_query": ([_vp, _vp, _u64, _vp, _vp], ctypes.c_int),
@@ -238,6 +265,20 @@ class Handle:
         assert hits.is_cuda and hits.dtype == torch.int32 and hits.is_contiguous() and hits.shape[0] >= n
         _check(_lib.vf_trace(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
                              self._flags(restart, persistent, incoherent), _stream_ptr(stream)))
+        return hits
+
+    def trace_scatter(self, rays, hits, slots, restart: bool = False, stream=None, incoherent: bool = False):
+        """vf_trace_scatter: the hit of ray i goes to row slots[i] of `hits` — a CUDA tensor, or a raw
+        device pointer (int) such as a peer process's frame buffer from ipc_open. slots: (n,) int32
+        CUDA tensor on the handle's device. Asynchronous on `stream`."""
+        import torch
+        n = rays.shape[0]
+        assert rays.is_cuda and rays.dtype == torch.float32 and rays.is_contiguous() and rays.shape[1] == 8
+        assert slots.is_cuda and slots.dtype == torch.int32 and slots.is_contiguous() and slots.shape[0] >= n
+        ptr = hits if isinstance(hits, int) else hits.data_ptr()
+        _check(_lib.vf_trace_scatter(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(ptr),
+                                     ctypes.c_void_p(slots.data_ptr()), self._flags(restart, False, incoherent),
+                                     _stream_ptr(stream)))
         return hits
 
     def trace_payload(self, rays, hits=None, payload=None, restart: bool = False, stream=None):

@@ -40,13 +40,15 @@ def test_multi_rank_code_path_with_one_rank():
     """bench.py's N > 1 path (NCCL group, max-over-ranks reductions, the chunked trace / NCCL hit
     gather pipeline of one tile-sharded frame, per-rank e2e) exercised on the one GPU of the box
     (--force-dist)."""
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-dist", "--config", "cfg2",
-                        "--no-cpu-baseline", "--no-side", "--steps", "3", "--warmup", "3", "--gather-chunks", "2"],
-                       capture_output=True, text=True, timeout=600, cwd=ROOT)
-    assert r.returncode == 0, r.stderr[-3000:]
-    d = json.loads([l for l in r.stdout.splitlines() if l.strip()][-1])
-    assert d["value"] > 0 and d["scaling"] == "strong" and d["gpu_launches"] == 6 and d["e2e"]["value"] > 0
-    assert d["trace_only"] >= 0.9 * d["value"]
+    for gather, launches in (("nccl", 6), ("p2p", 3)):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-dist", "--config", "cfg2",
+                            "--no-cpu-baseline", "--no-side", "--steps", "3", "--warmup", "3", "--gather-chunks", "2",
+                            "--gather", gather], capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert r.returncode == 0, r.stderr[-3000:]
+        d = json.loads([l for l in r.stdout.splitlines() if l.strip()][-1])
+        assert d["value"] > 0 and d["scaling"] == "strong" and d["gpu_launches"] == launches and d["e2e"]["value"] > 0
+        assert d["trace_only"] >= 0.9 * d["value"]
+        assert ("peer memory" in d["config"]["parallelism"]) == (gather == "p2p"), d["config"]["parallelism"]
 
 
 @pytest.mark.gpu

@@ -455,3 +455,25 @@ def test_align_nodes_parity_and_bytes(fmt, R_):
     ha.close()
     del keys, rgba
     torch.cuda.empty_cache()
+
+
+def test_trace_scatter_equals_trace_unpermuted():
+    """vf_trace_scatter (the fused trace + gather's kernel path) stores the hit of ray i at
+    slots[i]: on a local buffer with slots = the rays' pixel indices it must produce exactly
+    vf_trace's hits, un-permuted into pixel order (stack and restart; the ragged last tile
+    included: 72x40 pixels)."""
+    import torch
+    vf = _vf()
+    d = inputs.menger(128, 4)
+    keys, rgba = inputs.voxels_device(d)
+    h = vf.build((keys, rgba, (128,) * 3), "R(3^3) G(4)")
+    rays, perm = R.perspective(72, 40, 60.0, (-40.3, 60.7, -70.1), (40.5, 40.5, 40.5))
+    rt = torch.from_numpy(rays).cuda()
+    slots = torch.from_numpy(perm.astype(np.int32)).cuda()
+    for restart in (False, True):
+        ref = h.trace(rt, restart=restart).cpu().numpy()
+        frame = torch.full((len(rays), 4), 0x7F7F7F7F, dtype=torch.int32, device="cuda")
+        h.trace_scatter(rt, frame, slots, restart=restart)
+        out = frame.cpu().numpy()
+        assert np.array_equal(out[perm], ref)
+    h.close()

@@ -227,3 +227,34 @@ def test_bench_frame_step_gloo_world2():
     np.testing.assert_array_equal(img[:, 2], -pix)
     np.testing.assert_array_equal(img[:, 3], pix % 7)
     assert mx == [2.0, 10.0] and launches == 3
+
+
+@pytest.mark.gpu
+def test_p2p_fused_gather_two_processes(tmp_path):
+    """The fused trace + gather over peer memory (vf_trace_scatter into rank 0's frame, mapped by
+    CUDA IPC; shard.PeerFrame) with two real processes. The pool exposes one GPU, so both ranks
+    run on it: the IPC export / open / scatter path is the one NVLink peers take (cross-process
+    mapping, remote stores from the trace kernel). The assembled frame — row-major pixels, no
+    un-permutation — must equal the oracle's first hits pixel by pixel (cfg2, 1024x1024)."""
+    import subprocess
+    import sys
+    import oracle
+    import bench
+    from parity import assert_parity
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = _free_port()
+    out = str(tmp_path / "frame.npy")
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.join(root, "tests", "p2p_worker.py"), "cfg2", out],
+                                      env=env, cwd=root, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    logs = [p.communicate(timeout=600)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), "\n".join(l[-3000:] for l in logs)
+    frame = np.load(out)
+    rays, perm = bench.make_rays("cfg2")
+    g = oracle.Grid.from_generator(bench.make_volume("menger"))
+    ref = g.trace(rays)
+    g.close()
+    got = frame[perm]  # pixel order -> ray order
+    assert_parity(got[:, :3], got[:, 3].view(np.float32), ref, "cfg2 p2p two-process frame")
