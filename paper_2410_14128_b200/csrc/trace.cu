@@ -54,6 +54,13 @@ constexpr int TMIN_AXIS = 3;
 #ifndef VF_MINB_SPEC
 #define VF_MINB_SPEC 9  // compiled-in formats: 56 registers, 9 blocks per SM (A/B: +1.4-2.2 % over 8)
 #endif
+#ifndef VF_CHAIN_TOPNTREE
+#define VF_CHAIN_TOPNTREE 0  // restart descent chain for [R(A^3)] T(n, d) (A/B: -3 to -10 %)
+#endif
+#ifndef VF_CHAIN_TWOSPARSE
+#define VF_CHAIN_TWOSPARSE 1  // restart descent chain for S(a) G(b) without a Raw top (A/B: +5 to +11 %;
+                              // with R(4^3) on top -4 %)
+#endif
 #ifndef VF_MINB_CHAIN
 #define VF_MINB_CHAIN 8  // compiled-in chains of several Raw / DF levels
 #endif
@@ -331,7 +338,7 @@ struct NoSpec {
   static constexpr int kMinBlocks = VF_MINB;  // __launch_bounds__ min blocks per SM (register cap)
   static constexpr bool kIdx64 = true;        // Raw cell addresses may reach 2^32 words
   static constexpr bool kCacheGeom = false;   // compiled-in tier geometry cached in registers
-  static constexpr bool kChainRestart = true; // restart variant: descents chained before each step
+  static constexpr bool kChainRestart = false; // restart variant: descents chained before each step
   static constexpr uint32_t kTopWords = 0;  // words of a stageable top Raw grid (0: none)
 };
 
@@ -351,7 +358,7 @@ struct TopSparse {
   static constexpr int kMinBlocks = VF_MINB_SPEC;
   static constexpr bool kIdx64 = false;
   static constexpr bool kCacheGeom = false;
-  static constexpr bool kChainRestart = true;
+  static constexpr bool kChainRestart = KIND != K_NTREE || VF_CHAIN_TOPNTREE;  // A/B: restart +2.7 % cfg5, +8.8 % cfg4
   __device__ static __forceinline__ bool raw(int t) { return A > 0 && t == 0; }
   __device__ static __forceinline__ uint32_t lc(int t) { return LF * (uint32_t)(NT - 1 - t); }
   __device__ static __forceinline__ uint32_t msk(int t) { return raw(t) ? (1u << A) - 1u : (1u << LF) - 1u; }
@@ -390,7 +397,7 @@ struct RawChain {
 #define VF_CHAIN_CACHE 1
 #endif
   static constexpr bool kCacheGeom = NR > 1 && VF_CHAIN_CACHE;
-  static constexpr bool kChainRestart = NS > 0;  // only Raw levels: nothing to re-descend
+  static constexpr bool kChainRestart = false;  // A/B: R R G restart -1 to -4 % with the chain
   static constexpr uint32_t L2 = NS, L1 = NS + (NR > 2 ? A2 : 0u), L0 = L1 + (NR > 1 ? A1 : 0u);  // lc of raw tiers
   __host__ __device__ static constexpr uint32_t LCR(int t) { return t == 0 ? (NR == 1 ? NS : NR == 2 ? NS + A1 : L0) : t == 1 ? (NR == 2 ? NS : L1) : L2; }
   __device__ static __forceinline__ bool raw(int t) { return t < (int)NR; }
@@ -434,7 +441,7 @@ struct TwoSparse {
   static constexpr int kMinBlocks = VF_MINB_SPEC;
   static constexpr bool kIdx64 = false;
   static constexpr bool kCacheGeom = false;
-  static constexpr bool kChainRestart = true;
+  static constexpr bool kChainRestart = VF_CHAIN_TWOSPARSE && A == 0;
   __device__ static __forceinline__ bool raw(int t) { return A > 0 && t == 0; }
   __device__ static __forceinline__ uint32_t lc(int t) { return (uint32_t)(NT - 1 - t); }
   __device__ static __forceinline__ uint32_t msk(int t) { return raw(t) ? (1u << A) - 1u : 1u; }
@@ -466,7 +473,7 @@ struct SparseRaw {
   static constexpr int kMinBlocks = VF_MINB_SPEC;
   static constexpr bool kIdx64 = false;
   static constexpr bool kCacheGeom = false;
-  static constexpr bool kChainRestart = true;
+  static constexpr bool kChainRestart = false;  // A/B: cfg2 -10 %, cfg3 -16 % restart with the chain
   __device__ static __forceinline__ uint32_t lc(int t) { return t == (int)NS ? 0u : LC0 - LF * (uint32_t)t; }
   __device__ static __forceinline__ uint32_t msk(int t) { return t == (int)NS ? (1u << A) - 1u : (1u << LF) - 1u; }
   __device__ static __forceinline__ uint32_t sx(int t) { return t == (int)NS ? A : LF; }
@@ -917,7 +924,7 @@ struct Lane {
       return;
     }
     if ((S & (S - 1)) == 0) {
-      eaxis = __ffs(S) - 1;
+      eaxis = (S & 1) ? 0 : ((S & 2) ? 1 : 2);  // (selects: no BREV + FLO on the XU pipe)
       et = m;
     } else {
       const int res = argmin_exact(o[0], o[1], o[2], d[0], d[1], d[2], Pn[0], Pn[1], Pn[2], tn[0], tn[1], tn[2], S);
