@@ -3,7 +3,7 @@
 
 Default workload: cfg5 of BASELINE.json (`configs[4]`, the config the metric's "at 1/2/4/8 B200" is
 quoted on) — the 4096^3 sparse procedural volume (inputs.sparse, seed 0x4096), one 3840x2160
-perspective frame, format R(4^3) G(8) (the best hybrid of the cfg5 sweep, profiles/). A step = ONE
+perspective frame, format R(5^3) G(7) (the best hybrid of the cfg5 sweep, profiles/r2_pareto.md). A step = ONE
 FRAME: its rays are sharded over the N GPUs by interleaved 16x16 screen tiles (tile mod N; the
 volume is replicated on every GPU), every rank traces its tiles (all §8(a) rows run inside the one
 trace kernel) and the hits reach rank 0's frame buffer through the one collective (north_star,
@@ -14,7 +14,7 @@ N = 1 the frame is one trace launch. Total work is fixed as N grows ("scaling": 
 timed steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config cfg5] [--format "R(4^3) G(8)"] [--restart]
+                  [--config cfg5] [--format "R(5^3) G(7)"] [--restart]
                   [--sweep [--sweep-out FILE]] [--no-cpu-baseline] [--no-side]
 
 --gpus N > 1 outside torchrun re-launches itself under torch.distributed.run (one rank per GPU);
@@ -44,7 +44,7 @@ CONFIGS = {
     "cfg2": ("menger", "menger", "G(5) R(3, 3, 3)", "256^3 Menger sponge, 1024x1024 perspective rays"),
     "cfg3": ("terrain", "terrain", "T(2, 2) T(2, 1) R(4, 4, 4)", "1024^3 noise terrain/caves, 1920x1080 rays"),
     "cfg4": ("city", "city", "R(4, 4, 4) G(7)", "2048^3 synthetic city blocks, 1920x1080 aerial rays"),
-    "cfg5": ("sparse", "sparse", "R(4, 4, 4) G(8)",
+    "cfg5": ("sparse", "sparse", "R(5, 5, 5) G(7)",
              "4096^3 sparse procedural shells, 3840x2160 rays tile-sharded over the GPUs"),
     # incoherent secondary-style rays through the cfg4 city (not a BASELINE config)
     "cfg4i": ("city", "incoherent", "R(4, 4, 4) G(7)",
@@ -64,9 +64,10 @@ SWEEP = {
     "cfg4": ["R(4, 4, 4) G(7)", "R(3, 3, 3) G(8)", "G(11)", "S(11)", "R(6, 6, 6) G(5)", "R(8, 8, 8) G(3)",
              "R(4, 4, 4) S(7)", "R(6, 6, 6) S(5)", "S(3) G(8)", "S(5) G(6)", "S(7) G(4)", "R(4, 4, 4) R(3, 3, 3) G(4)",
              "R(4, 4, 4) S(3) G(4)", "R(4, 4, 4) R(4, 4, 4) R(3, 3, 3)", "R(1, 1, 1) T(2, 5)", "T(2, 4) R(3, 3, 3)",
-             "T(2, 2) T(2, 2) R(3, 3, 3)", "T(2, 3) R(5, 5, 5)"],
-    "cfg5": ["R(4, 4, 4) G(8)", "R(3, 3, 3) G(9)", "G(12)", "T(2, 6)", "S(12)", "R(4, 4, 4) T(2, 4)",
-             "R(4, 4, 4) R(4, 4, 4) R(4, 4, 4)"],
+             "T(2, 2) T(2, 2) R(3, 3, 3)", "T(2, 3) R(5, 5, 5)", "R(5, 5, 5) G(6)", "D(5, 5, 5, 6) G(6)"],
+    "cfg5": ["R(5, 5, 5) G(7)", "R(4, 4, 4) G(8)", "R(3, 3, 3) G(9)", "G(12)", "T(2, 6)", "S(12)", "R(4, 4, 4) T(2, 4)",
+             "R(4, 4, 4) R(4, 4, 4) R(4, 4, 4)", "D(4, 4, 4, 6) G(8)", "D(3, 3, 3, 6) G(9)", "D(5, 5, 5, 6) G(7)",
+             "R(6, 6, 6) G(6)", "D(6, 6, 6, 6) G(6)", "R(7, 7, 7) G(5)"],
 }
 # PAPER.md Table 2 (tests/golden/table2_formats.txt): rows 1-20 on cfg4, rows 21-40 on t512
 _T2 = [l.strip().split(" ", 2) for l in open(os.path.join(ROOT, "tests", "golden", "table2_formats.txt"))
@@ -303,7 +304,23 @@ class FrameStep:
     def _trace(self, lo, hi, hv):
         self._timed(self.trace, self.rays[lo:hi], hv)
 
+    def capture(self):
+        """Single-rank frame: capture its one trace launch in a CUDA graph, replayed by every later
+        call (no per-step host launch cost between the step's events; the step time is then the
+        kernel's own time)."""
+        import torch
+        if self.pipe is not None or self.peer is not None:
+            return
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.trace(self.rays[:self.n_local], self.hits)
+        torch.cuda.synchronize()
+
     def __call__(self):
+        if getattr(self, "graph", None) is not None:
+            self.graph.replay()
+            return None
         if self.peer is not None:
             return self.peer.run(lambda r, ptr, sl: self._timed(self.trace_scatter, r, ptr, sl), self.rays)
         if self.pipe is None:
@@ -317,8 +334,12 @@ class FrameStep:
             return self.peer.frame[self.peer.slots.long()] if self.peer.frame is not None else None
         return self.hits[:self.n_local]
 
-    def kernel_ms(self):
-        """Sum of the trace launches' CUDA-event durations since the last call (then reset)."""
+    def kernel_ms(self, step_ms=None):
+        """Sum of the trace launches' CUDA-event durations since the last call (then reset); for a
+        graph-replayed single launch, the steps' own event times (the step is that one kernel)."""
+        if getattr(self, "graph", None) is not None and step_ms is not None:
+            self.kernel_events = []
+            return sum(step_ms)
         ms = sum(a.elapsed_time(b) for a, b in self.kernel_events)
         self.kernel_events = []
         return ms
@@ -451,6 +472,8 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     step.kernel_ms()
+    step.capture()  # N = 1: the frame's one launch replayed as a CUDA graph
+    step()
     if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
@@ -471,7 +494,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    kern_ms = step.kernel_ms() / args.steps  # this rank's trace launches per step
+    kern_ms = step.kernel_ms(step_ms) / args.steps  # this rank's trace launches per step
     tot_ms, kern_max = max_over_ranks([sum(step_ms), kern_ms], dev, dist_on)
     value = n_total * args.steps / (tot_ms / 1e3) / 1e6
 

@@ -1412,7 +1412,8 @@ KernelFn select_spec(const Format& f, bool restart, int mode, bool aln) {
 #define VF_SPECA(a, m) /* + the VF_BUILD_ALIGN_NODES instance */ \
   case ((a) << 8) | (m): return spec_kernel<5, RawSvdag<a, m>, true>(restart, mode, aln);
         VF_SPECA(4, 7) VF_SPECA(4, 8) VF_SPECA(3, 8) VF_SPEC(3, 7) VF_SPEC(4, 5) VF_SPEC(2, 7) VF_SPEC(6, 5)
-        VF_SPEC(8, 3) VF_SPEC(3, 5) VF_SPECA(3, 9) VF_SPEC(7, 2)
+        VF_SPEC(8, 3) VF_SPEC(3, 5) VF_SPECA(3, 9) VF_SPEC(7, 2) VF_SPEC(5, 7) VF_SPEC(5, 6)
+        VF_SPEC(6, 6) VF_SPEC(7, 5)
         VF_SPECA(2, 3) VF_SPEC(1, 4)  // small instances for the parity tests
 #undef VF_SPEC
 #undef VF_SPECA
@@ -1440,6 +1441,8 @@ KernelFn select_spec(const Format& f, bool restart, int mode, bool aln) {
     return spec_kernel<(1u << K_RAW) | (1u << K_OF_##k), TopSparse<a, K_OF_##k, 1, ns, true>>(restart, mode);
       VF_DS(4, VF_SVDAG, 7) VF_DS(6, VF_SVDAG, 5) VF_DS(4, VF_SVO, 7) VF_DS(6, VF_SVO, 5) VF_DS(4, VF_SVDAG, 5)
       VF_DS(4, VF_SVO, 5) VF_DS(2, VF_SVDAG, 2)
+      VF_DS(4, VF_SVDAG, 8) VF_DS(5, VF_SVDAG, 7) VF_DS(3, VF_SVDAG, 9) VF_DS(5, VF_SVDAG, 6)  // cfg5 / cfg4 DF hybrids
+      VF_DS(6, VF_SVDAG, 6) VF_DS(7, VF_SVDAG, 5)
 #undef VF_DS
 #define VF_TSA(a, k, lf, ns, kinds) /* + the VF_BUILD_ALIGN_NODES instance */ \
   case ((a) << 24) | ((k) << 16) | ((lf) << 8) | (ns): \

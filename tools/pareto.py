@@ -1,10 +1,12 @@
 """Pareto frontier (fig:figure_1/2: rendering performance vs storage size, lower
 bytes and higher Mrays/s better) of a bench.py JSON line's format sweep, stack variant, plus the
-restart-sv gain per format (fig:restart-sv). usage: python tools/pareto.py BENCH_JSON"""
+restart-sv gain per format (fig:restart-sv). usage: python tools/pareto.py BENCH_JSON [SWEEP_JSON]"""
 import json
 import sys
 
 d = json.loads(open(sys.argv[1]).read().strip().split("\n")[-1])
+if len(sys.argv) > 2:  # bench.py --sweep --sweep-out FILE
+    d["sweep"] = json.load(open(sys.argv[2]))["rows"]
 rows = [r for r in d.get("sweep", []) if "mrays_s" in r]
 stack = {r["format"]: r for r in rows if r["variant"] == "stack"}
 restart = {r["format"]: r for r in rows if r["variant"] == "restart"}

@@ -20,11 +20,13 @@ ap.add_argument("--format", default=None)
 ap.add_argument("--restart", action="store_true")
 ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--counters", action="store_true")
+ap.add_argument("--align", action="store_true", help="build with VF_BUILD_ALIGN_NODES")
 a = ap.parse_args()
 vname, _, deffmt, _ = bench.CONFIGS[a.config]
 vol = bench.make_volume(vname)
 keys, rgba = inputs.voxels_device(vol)
-h = vf.build((keys, rgba, inputs.dims_of(vol)), a.format or deffmt)
+h = vf.build((keys, rgba, inputs.dims_of(vol)), a.format or deffmt,
+             flags=vf.VF_BUILD_DEFAULT | (vf.VF_BUILD_ALIGN_NODES if a.align else 0))
 del keys, rgba
 rays_np, _ = bench.make_rays(a.config)
 rays = torch.from_numpy(rays_np).cuda()

@@ -7,7 +7,7 @@ if len(sys.argv) > 2:  # bench.py --sweep --sweep-out FILE: the rows live in the
     d["sweep"] = json.load(open(sys.argv[2]))["rows"]
 print(f"## {d['config']['workload']}\n")
 print(f"headline: {d['config']['format']} {d['config']['variant']}: {d['value']} Mrays/s "
-      f"({d['ms_per_step']} ms/frame, {d['config']['rays']} rays), e2e {d['e2e']['value']} Mrays/s; "
+      f"({d['ms_per_step']} ms/frame, {d['config'].get('rays_per_frame', d['config'].get('rays'))} rays), e2e {d['e2e']['value']} Mrays/s; "
       f"clocks {d.get('clocks')}\n")
 cb = d.get("cpu_baseline") or {}
 if cb:
