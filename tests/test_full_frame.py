@@ -108,7 +108,7 @@ def test_cfg4s_secondary_full_frame():
 
 
 def test_cfg5_full_frame_every_sweep_format():
-    """cfg5 (4096^3, 3840x2160 = 8,294,400 rays): the bench's headline R(4^3) G(8) and every other
+    """cfg5 (4096^3, 3840x2160 = 8,294,400 rays): the bench's headline R(5^3) G(7) and every other
     format of the cfg5 sweep, each over the whole frame, stack and restart."""
     import bench
     _check("cfg5", bench.SWEEP["cfg5"])

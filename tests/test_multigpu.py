@@ -258,3 +258,53 @@ def test_p2p_fused_gather_two_processes(tmp_path):
     g.close()
     got = frame[perm]  # pixel order -> ray order
     assert_parity(got[:, :3], got[:, 3].view(np.float32), ref, "cfg2 p2p two-process frame")
+
+
+def _peer_worker(rank, world, port, fail_rank, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2410_14128_b200 import shard
+    import paper_2410_14128_b200.vf as vfm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # the CUDA IPC calls are stubbed: this checks PeerFrame's host protocol (export on rank 0,
+    # broadcast, open elsewhere, every rank agreeing on failure), not the mapping itself
+    vfm.ipc_export = lambda t: b"H" * 72
+    def _open(blob, dev):
+        if rank == fail_rank:
+            raise RuntimeError("no peer access")
+        assert blob == b"H" * 72
+        return 0x1000 + rank
+    vfm.ipc_open = _open
+    vfm.ipc_close = lambda p: None
+    try:
+        pf = shard.PeerFrame(10, np.arange(3) + rank, torch.device("cpu"))
+        res = ("ok", pf.ptr if rank else -1, pf.slots.tolist(), pf.frame is not None)
+    except RuntimeError as e:
+        res = ("failed", str(e))
+    q.put((rank, res))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [None, 1])
+def test_peer_frame_protocol_gloo(fail_rank):
+    """shard.PeerFrame's host protocol at world size 2 over gloo: rank 0 exports its frame buffer,
+    the handle is broadcast, rank 1 maps it; if the mapping fails on any rank, EVERY rank raises
+    (so bench.py's FrameStep falls back to the NCCL gather together)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, fail_rank, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    if fail_rank is None:
+        assert got[0] == ("ok", -1, [0, 1, 2], True)
+        assert got[1] == ("ok", 0x1001, [1, 2, 3], False)
+    else:
+        assert all(r[0] == "failed" and "no peer access" in r[1] for r in got.values()), got
