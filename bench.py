@@ -471,9 +471,10 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    step.kernel_ms()
     step.capture()  # N = 1: the frame's one launch replayed as a CUDA graph
     step()
+    torch.cuda.synchronize()
+    step.kernel_ms()  # reset: only the timed steps' launches count
     if dist_on:
         dist.barrier()
     torch.cuda.synchronize()

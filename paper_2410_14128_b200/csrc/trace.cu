@@ -1351,12 +1351,15 @@ KernelFn select_kernel(uint32_t kinds, bool restart, bool count, bool persistent
 // Compiled-in formats: R(A^3) G(M) (RawSvdag: the cfg4 / cfg5 / t512 headline formats and their
 // sweep neighbours) and the cfg2 / cfg3 headline formats (SparseRaw). Others run the generic kernel.
 // mode 0: one thread per ray; 1: chunked persistent warps; 2: chunked + top Raw grid in shared memory
-// ALNOK: the format also gets the VF_BUILD_ALIGN_NODES instance (aligned SVDAG header loads)
-template <uint32_t KINDS, class D, bool ALNOK = false>
+// HEADLINE: the format also gets the VF_BUILD_ALIGN_NODES instance (aligned SVDAG header loads) and
+// the counting instance (mode -1: vf_trace_counters runs the same compiled-in traversal it counts)
+template <uint32_t KINDS, class D, bool HEADLINE = false>
 KernelFn spec_kernel(bool restart, int mode, bool aln = false) {
-  if constexpr (ALNOK) {
+  if constexpr (HEADLINE) {
+    if (mode == -1) return restart ? trace_kernel<KINDS, true, true, D> : trace_kernel<KINDS, false, true, D>;
     if (aln && mode == 0) return restart ? trace_kernel<KINDS, true, false, D, true> : trace_kernel<KINDS, false, false, D, true>;
   }
+  if (mode < 0) return nullptr;  // counting: the generic kernel
   (void)aln;
 #ifdef VF_CHUNKED_KERNELS
   if constexpr (D::kTopWords != 0) {
@@ -1410,10 +1413,10 @@ KernelFn select_spec(const Format& f, bool restart, int mode, bool aln) {
     if (e[0] == e[1] && e[1] == e[2]) switch (((uint32_t)e[0] << 8) | f.levels[1].depth) {
 #define VF_SPEC(a, m) \
   case ((a) << 8) | (m): return spec_kernel<5, RawSvdag<a, m>>(restart, mode);
-#define VF_SPECA(a, m) /* + the VF_BUILD_ALIGN_NODES instance */ \
+#define VF_SPECA(a, m) /* + the VF_BUILD_ALIGN_NODES and counting instances */ \
   case ((a) << 8) | (m): return spec_kernel<5, RawSvdag<a, m>, true>(restart, mode, aln);
         VF_SPECA(4, 7) VF_SPECA(4, 8) VF_SPECA(3, 8) VF_SPEC(3, 7) VF_SPEC(4, 5) VF_SPEC(2, 7) VF_SPEC(6, 5)
-        VF_SPEC(8, 3) VF_SPEC(3, 5) VF_SPECA(3, 9) VF_SPEC(7, 2) VF_SPEC(5, 7) VF_SPEC(5, 6)
+        VF_SPEC(8, 3) VF_SPEC(3, 5) VF_SPECA(3, 9) VF_SPEC(7, 2) VF_SPECA(5, 7) VF_SPEC(5, 6)
         VF_SPEC(6, 6) VF_SPEC(7, 5)
         VF_SPECA(2, 3) VF_SPEC(1, 4)  // small instances for the parity tests
 #undef VF_SPEC
@@ -1445,7 +1448,7 @@ KernelFn select_spec(const Format& f, bool restart, int mode, bool aln) {
       VF_DS(4, VF_SVDAG, 8) VF_DS(5, VF_SVDAG, 7) VF_DS(3, VF_SVDAG, 9) VF_DS(5, VF_SVDAG, 6)  // cfg5 / cfg4 DF hybrids
       VF_DS(6, VF_SVDAG, 6) VF_DS(7, VF_SVDAG, 5)
 #undef VF_DS
-#define VF_TSA(a, k, lf, ns, kinds) /* + the VF_BUILD_ALIGN_NODES instance */ \
+#define VF_TSA(a, k, lf, ns, kinds) /* + the VF_BUILD_ALIGN_NODES and counting instances */ \
   case ((a) << 24) | ((k) << 16) | ((lf) << 8) | (ns): \
     return spec_kernel<kinds, TopSparse<a, K_OF_##k, lf, ns>, true>(restart, mode, aln);
       VF_TSA(0, VF_SVDAG, 1, 11, 4) VF_TS(0, VF_SVO, 1, 11, 2) VF_TSA(0, VF_SVDAG, 1, 8, 4) VF_TS(0, VF_SVO, 1, 8, 2)
@@ -1527,9 +1530,9 @@ KernelFn select_spec(const Format& f, bool restart, int mode, bool aln) {
       default: break;
     }
   }
-  if (same_format(f, kFmtG5R3)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 3, 0x10, 0x1>>(restart, mode);
+  if (same_format(f, kFmtG5R3)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 5, 3, 0x10, 0x1>, true>(restart, mode);
   if (same_format(f, kFmtG2R2)) return spec_kernel<5, SparseRaw<K_SVDAG, 1, 2, 2, 0x2, 0x1>>(restart, mode);
-  if (same_format(f, kFmtT22T21R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x6, 0x5>>(restart, mode);
+  if (same_format(f, kFmtT22T21R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x6, 0x5>, true>(restart, mode);
   if (same_format(f, kFmtT21T22R4)) return spec_kernel<9, SparseRaw<K_NTREE, 2, 3, 4, 0x5, 0x3>>(restart, mode);
   if (same_format(f, kFmtT11T12R1)) return spec_kernel<9, SparseRaw<K_NTREE, 1, 3, 1, 0x5, 0x3>>(restart, mode);
   if (same_format(f, kFmtS5R5)) return spec_kernel<3, SparseRaw<K_SVO, 1, 5, 5, 0x10, 0x1>>(restart, mode);
@@ -1592,6 +1595,9 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
       fn = sf;
       chunked = mode > 0;
     }
+  // counting runs of the headline formats use their compiled-in traversal too (same code as timed)
+  if (!persistent && counters && !no_spec)
+    if (KernelFn sf = select_spec(h->fmt, (flags & VF_TRACE_RESTART_SV) != 0, -1, false)) fn = sf;
   if (!fn) {
     set_error("vf_trace: no kernel instantiated for kind set 0x%x", kinds);
     return VF_ERR_UNSUPPORTED;

@@ -477,3 +477,43 @@ def test_trace_scatter_equals_trace_unpermuted():
         out = frame.cpu().numpy()
         assert np.array_equal(out[perm], ref)
     h.close()
+
+
+_COUNT_CHILD = r'''
+import json, os, sys
+import numpy as np, torch
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+import inputs
+from inputs import rays as R
+from paper_2410_14128_b200 import vf
+kind, fmt = sys.argv[1], sys.argv[2]
+d = inputs.random_occupancy((32,) * 3, 0.05, 0xC0) if kind == "rand" else inputs.menger(256, 5)
+dims = inputs.dims_of(d)
+keys, rgba = inputs.voxels_device(d)
+h = vf.build((keys, rgba, dims), fmt)
+rays = np.concatenate([R.adversarial_rays(3000, dims, 71), R.random_rays(3000, dims, 72)])
+rt = torch.from_numpy(rays).cuda()
+print(json.dumps([h.counters(rt, restart=r) for r in (False, True)]))
+'''
+
+
+@pytest.mark.parametrize("kind,fmt", [("rand", "R(2^3) G(3)"), ("menger", "G(5) R(3^3)")])
+def test_counting_runs_the_compiled_in_traversal(kind, fmt):
+    """vf_trace_counters of a headline format runs the compiled-in kernel (the code bench.py times),
+    and every per-ray counter (cells, steps, descents, format bytes, sector reads, distinct words,
+    exact fallbacks) equals the generic tier-table kernel's (VF_NO_SPEC=1) on the same rays."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_extra in ({}, {"VF_NO_SPEC": "1"}):
+        env = dict(os.environ, ROOT=root, **env_extra)
+        env.pop("VF_NO_SPEC", None) if not env_extra else None
+        r = subprocess.run([sys.executable, "-c", _COUNT_CHILD, kind, fmt], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
+    assert outs[0][0]["cell_tests"] > 0 and outs[0][1]["redescents"] >= 0
