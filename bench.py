@@ -458,7 +458,7 @@ def run_ours(args):
     rays = torch.from_numpy(np.ascontiguousarray(rays_all[own])).to(dev)
     stream = torch.cuda.current_stream()
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
-    incoh = CONFIGS[cfg][1] in ("incoherent", "secondary")  # VF_TRACE_INCOHERENT hint
+    incoh = CONFIGS[cfg][1] == "incoherent"  # VF_TRACE_INCOHERENT hint (not for cfg4s: its screen-ordered secondary rays are coherent enough, plain kernel +36 %)
 
     def trace(rv, hv):
         handle.trace(rv, hv, restart=args.restart, incoherent=incoh)
@@ -614,7 +614,7 @@ def sweep(cfg, vol, rays, hits, stream, flush, args):
     g, _, _ = oracle_grid(vol)
     ref = g.trace(rays.cpu().numpy()[idx])
     g.close()
-    incoh = CONFIGS[cfg][1] in ("incoherent", "secondary")
+    incoh = CONFIGS[cfg][1] == "incoherent"
     out = []
     for fmt in SWEEP[cfg]:
         try:

@@ -84,8 +84,9 @@ def test_cfg4s_secondary_full_frame():
     """SURVEY §8(f) NEXT 3 as specified: shadow + AO rays spawned from the cfg4 primary hits
     (inputs.rays.secondary; origin on the entry face from the hit voxel / t / entry-face normal).
     The spawn inputs are the ORACLE's primary hits (never the CUDA path's); every secondary ray of
-    the frame is traced on the GPU in bench.py's launch configuration (VF_TRACE_INCOHERENT hint)
-    and compared with the oracle, for every format of the cfg4s sweep, stack and restart."""
+    the frame is traced on the GPU in bench.py's launch configuration (plain kernel) and with the
+    VF_TRACE_INCOHERENT kernel, and compared with the oracle, for every format of the cfg4s sweep,
+    stack and restart."""
     import bench
     import torch
     from inputs import rays as R
@@ -102,9 +103,11 @@ def test_cfg4s_secondary_full_frame():
     hits = torch.empty((len(rays), 4), dtype=torch.int32, device="cuda")
     for fmt, h in _handles(vol, bench.SWEEP["cfg4s"]):
         for restart in (False, True):
-            h.trace(rt, hits, restart=restart, incoherent=True)
-            out = hits.cpu().numpy()
-            assert_parity(out[:, :3], out[:, 3].view(np.float32), ref, f"cfg4s {fmt} restart={restart} (full frame)")
+            for incoh in (False, True):  # bench.py's launch (plain) and the VF_TRACE_INCOHERENT kernel
+                h.trace(rt, hits, restart=restart, incoherent=incoh)
+                out = hits.cpu().numpy()
+                assert_parity(out[:, :3], out[:, 3].view(np.float32), ref,
+                              f"cfg4s {fmt} restart={restart} incoherent={incoh} (full frame)")
 
 
 def test_cfg5_full_frame_every_sweep_format():

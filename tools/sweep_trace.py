@@ -16,7 +16,7 @@ vol = bench.make_volume(bench.CONFIGS[cfg][0])
 k, c = inputs.voxels_device(vol)
 rays = torch.from_numpy(bench.make_rays(cfg)[0]).cuda()
 hits = torch.empty((rays.shape[0], 4), dtype=torch.int32, device="cuda")
-incoh = bench.CONFIGS[cfg][1] in ("incoherent", "secondary")
+incoh = bench.CONFIGS[cfg][1] == "incoherent"
 for fmt in bench.SWEEP[cfg]:
     h = vf.build((k, c, inputs.dims_of(vol)), fmt)
     for restart in (False, True):
