@@ -328,6 +328,13 @@ class FrameStep:
             return None
         return self.pipe.run(self._trace)
 
+    def launches_per_step(self, count):
+        """Kernel launches of one step: count(ray view) per trace call (vf_trace_launch_count: 3 when
+        VF_TRACE_SCHEDULE reorders the call, else 1)."""
+        if self.pipe is None:
+            return count(self.rays[:self.n_local])
+        return sum(count(self.rays[lo:hi]) for lo, hi in self.pipe.bounds)
+
     def local_hits(self):
         """This rank's hits in its own ray order (rank 0 only in p2p mode)."""
         if self.peer is not None:
@@ -389,22 +396,29 @@ def side_cfg4(args, stream, flush):
     rays_np, _ = make_rays("cfg4")
     rays = torch.from_numpy(np.ascontiguousarray(rays_np)).cuda()
     hits = torch.empty((rays.shape[0], 4), dtype=torch.int32, device="cuda")
-    for _ in range(3):
-        h.trace(rays, hits, restart=args.restart)
-    ms = []
-    for i in range(max(args.steps, 5)):
-        flush.fill_(i)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        h.trace(rays, hits, restart=args.restart)
-        b.record(stream)
-        ms.append((a, b))
-    torch.cuda.synchronize()
-    t = statistics.mean(a.elapsed_time(b) for a, b in ms)
+    sched = args.schedule == "on"
+
+    def timed(schedule):
+        for _ in range(3):
+            h.trace(rays, hits, restart=args.restart, schedule=schedule)
+        ms = []
+        for i in range(max(args.steps, 5)):
+            flush.fill_(i)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            h.trace(rays, hits, restart=args.restart, schedule=schedule)
+            b.record(stream)
+            ms.append((a, b))
+        torch.cuda.synchronize()
+        return statistics.mean(a.elapsed_time(b) for a, b in ms)
+
+    t = timed(sched)
+    t_nat = timed(False) if sched else t
     st = h.stats()
     h.close()
     return {"workload": "cfg4: 2048^3 city, 1920x1080 aerial", "format": "R(4^3) G(7)",
             "value": round(rays.shape[0] / (t / 1e3) / 1e6, 1), "unit": "Mrays/s", "kernel_ms": round(t, 4),
+            "index_order_value": round(rays.shape[0] / (t_nat / 1e3) / 1e6, 1),
             "bytes_per_voxel": round(st["bytes_used"] / nonempty, 4)}
 
 
@@ -460,11 +474,13 @@ def run_ours(args):
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
     incoh = CONFIGS[cfg][1] == "incoherent"  # VF_TRACE_INCOHERENT hint (not for cfg4s: its screen-ordered secondary rays are coherent enough, plain kernel +36 %)
 
+    sched = args.schedule == "on" and not incoh  # VF_TRACE_SCHEDULE (coherent launches only)
+
     def trace(rv, hv):
-        handle.trace(rv, hv, restart=args.restart, incoherent=incoh)
+        handle.trace(rv, hv, restart=args.restart, incoherent=incoh, schedule=sched)
 
     def trace_scatter(rv, ptr, slots):
-        handle.trace_scatter(rv, ptr, slots, restart=args.restart, incoherent=incoh)
+        handle.trace_scatter(rv, ptr, slots, restart=args.restart, incoherent=incoh, schedule=sched)
 
     step = FrameStep(trace, rays, counts, rank, world, dist_on, dev, args.gather_chunks,
                      trace_scatter=trace_scatter, pixels_local=perm[own], n_total=n_total, gather=args.gather)
@@ -500,7 +516,8 @@ def run_ours(args):
     value = n_total * args.steps / (tot_ms / 1e3) / 1e6
 
     # ---- end to end through the public API with HOST buffers: every rank copies its shard's rays
-    # from pinned host memory, traces and copies the hits back (vf_trace_host); the ranks share the
+    # from pinned host memory, traces and copies the hits back (vf_trace_host; PCIe-bound, so its
+    # chunks run in index order, no VF_TRACE_SCHEDULE); the ranks share the
     # node's host memory, so the frame's hits land on the host with no device collective. Time per
     # frame = max over ranks.
     hr = torch.from_numpy(np.ascontiguousarray(rays_all[own])).pin_memory()
@@ -570,6 +587,8 @@ def run_ours(args):
                        "bytes_per_voxel_paper": round(stats["paper_layout_bytes"] / nonempty, 4),
                        "hit_rate": round(float((gxyz[:, 0] >= 0).mean()), 4), "build_s": round(build_s, 3),
                        "voxel_gen_s": round(gen_s, 2), "l2": "flushed between timed steps (2x126 MB write)",
+                       "schedule": ("longest-first block order from the previous frame's per-block durations "
+                                    "(VF_TRACE_SCHEDULE; same camera every frame)") if sched else "index order",
                        "parallelism": f"tile{world}: one frame's 16x16 tiles interleaved over {world} GPU(s), volume "
                                       f"replicated" + (
                                           ", fused trace + hit scatter into rank 0's frame over peer memory (CUDA IPC)"
@@ -578,10 +597,25 @@ def run_ours(args):
                                           if dist_on else "") + (f" [{step.gather_note}]" if step.gather_note else "")},
             "e2e": {"value": round(e2e_val, 1), "unit": "Mrays/s", "h2d_bytes_per_step": n_total * 32,
                     "d2h_bytes_per_step": n_total * 16},
-            "gpu_launches": step.launches * args.steps,
+            "gpu_launches": args.steps * step.launches_per_step(
+                lambda v: handle.launch_count(v, restart=args.restart, incoherent=incoh, schedule=sched)),
             "roofline": roof, "issue_roofline": issue, "cpu_baseline": cpu, "clocks": clk,
             "trace_only": round(n_total / (kern_max / 1e3) / 1e6, 1),
         }
+        if world == 1 and sched:
+            # the same frame with the blocks in index order (no schedule), for comparison
+            nat = []
+            hv = step.hits
+            for i in range(max(5, min(args.steps, 10))):
+                flush.fill_(i)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                handle.trace(rays, hv, restart=args.restart, incoherent=incoh)
+                b.record(stream)
+                nat.append((a, b))
+            torch.cuda.synchronize()
+            nat_ms = statistics.median(a.elapsed_time(b) for a, b in nat)
+            result["index_order"] = {"value": round(n_total / (nat_ms / 1e3) / 1e6, 1), "kernel_ms": round(nat_ms, 4)}
         if world == 1 and not args.no_side and cfg != "cfg4":
             result["cfg4_2048"] = side_cfg4(args, stream, flush)
         if args.sweep and world == 1 and cfg in SWEEP:
@@ -741,6 +775,8 @@ def main(argv=None):
     ap.add_argument("--gather-chunks", type=int, default=0, help="N>1 nccl gather: trace/gather pipeline depth (0: auto)")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="N>1: fused trace + peer-memory hit scatter (p2p) or trace + NCCL gather")
+    ap.add_argument("--schedule", default="on", choices=["on", "off"],
+                    help="VF_TRACE_SCHEDULE: blocks ordered by the previous frame's block durations")
     ap.add_argument("--force-dist", action="store_true", help="test aid: the N>1 code path with one rank")
     argv = sys.argv[1:] if argv is None else argv
     args = ap.parse_args(argv)

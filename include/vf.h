@@ -181,6 +181,23 @@ enum {
                                    with new rays (one atomic per batch), recovering the SIMT lanes
                                    a warp otherwise idles while its longest ray finishes. Results
                                    are identical; coherent primary rays are faster without it. */
+  VF_TRACE_SCHEDULE = 1u << 2,   /* longest-first block schedule (list scheduling, LPT): every
+                                   launch with this flag records the duration of each of its
+                                   128-ray blocks, and a later such launch on the same handle
+                                   with the SAME ray pointer and count (the next frame of a
+                                   renderer reusing its ray buffer) starts its blocks in order of
+                                   decreasing recorded duration, so the slow blocks no longer
+                                   start last and the launch tail shrinks. Only the order in which
+                                   blocks run changes: every ray is traced, results are identical.
+                                   The first launch over an array runs in index order, and so does
+                                   every launch of at most two waves of resident blocks (nothing to
+                                   reorder). The handle
+                                   keeps 8 B per block for up to 32 arrays (least recently used
+                                   evicted; allocated through the build's vf_allocator); launches
+                                   sharing an array are ordered by an event (inside stream capture
+                                   the graph orders them, and an array first seen during capture
+                                   runs unscheduled). Coherent-ray launches only (not with
+                                   VF_TRACE_INCOHERENT, whose persistent warps balance by design). */
   /* bit 30 is reserved (internal ablation: persistent warps with dynamic ray refill) */
 };
 
@@ -193,6 +210,12 @@ enum {
  * Results are identical (environment VF_NO_SPEC=1 forces the generic kernel). */
 VF_API vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t trace_flags,
                    void* cuda_stream);
+
+/* Kernel launches one vf_trace / vf_trace_ex / vf_trace_scatter call with these arguments makes
+ * now (host-side query, no GPU work): 3 when VF_TRACE_SCHEDULE will reorder it (the two order
+ * kernels + the trace), else 1. For launch accounting (bench.py's gpu_launches). */
+VF_API vf_status vf_trace_launch_count(const vf_handle* h, const vf_ray* rays, uint64_t n, uint32_t trace_flags,
+                                       uint32_t* count);
 
 /* Closest-hit payload (the paper's closest-hit shader):
  * rgba = the hit voxel's stored word (its RGBA; 0 on a miss); normal = the entry

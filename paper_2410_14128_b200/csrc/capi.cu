@@ -151,6 +151,17 @@ vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* h
   return launch_trace(h, rays, n, hits, trace_flags, (cudaStream_t)cuda_stream);
 }
 
+vf_status vf_trace_launch_count(const vf_handle* h, const vf_ray* rays, uint64_t n, uint32_t trace_flags,
+                                uint32_t* count) {
+  clear_error();
+  if (!h || !count) {
+    set_error("vf_trace_launch_count: null argument");
+    return VF_ERR_INVALID_ARG;
+  }
+  *count = trace_launch_count(h, rays, n, trace_flags);
+  return VF_OK;
+}
+
 vf_status vf_trace_ex(const vf_handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, vf_payload* payload,
                       uint32_t trace_flags, void* cuda_stream) {
   clear_error();
@@ -424,6 +435,7 @@ void vf_destroy(vf_handle* h) {
   if (!h) return;
   DeviceGuard g(h->device);
   cudaDeviceSynchronize();  // no kernel or copy of this handle may still use its memory
+  free_schedules(h);
   h->alloc.put(h->buf, h->buf_bytes, h->build_stream);
   h->alloc.put(h->stage, h->stage_bytes, h->build_stream);
   h->alloc.put(h->work, sizeof(unsigned long long) * 2 * kWorkSlots, h->build_stream);

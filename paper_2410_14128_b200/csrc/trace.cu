@@ -34,10 +34,13 @@
 // returns the same voxel, bit for bit.
 #include <stdint.h>
 
+#include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <mutex>
 #include <type_traits>
+#include <vector>
 
 #include "vf_internal.cuh"
 
@@ -1043,14 +1046,25 @@ __device__ __forceinline__ void stage_tiers(const TraceParams& p, uint32_t* s_tw
 #define VF_TRACE_THREADS 128  // block size (A/B: 256 with VF_MINB 4 keeps the 64-register cap)
 #endif
 constexpr unsigned kTraceThreads = VF_TRACE_THREADS;
+#ifdef VF_BLOCK_CLOCK
+__device__ unsigned long long* g_block_clock;
+#endif
 template <uint32_t KINDS, bool RESTART, bool COUNT, class D = NoSpec, bool ALN = false>
 __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(const TraceParams p, const uint32_t* __restrict__ buf,
                                                     const float4* __restrict__ rays, int4* __restrict__ hits,
                                                     uint64_t n, unsigned long long* __restrict__ counters,
                                                     unsigned long long* __restrict__ work) {
   __shared__ __align__(16) uint32_t s_tw[8 * VF_MAX_TIERS];
+  __shared__ long long s_clk;  // VF_TRACE_SCHEDULE: the block's start (SM cycles)
+#ifdef VF_BLOCK_CLOCK  // analysis build (tools/block_timeline.py): per-block start / end / SM
+  unsigned long long blk_t0 = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(blk_t0));
+#endif
+  if (p.cost && threadIdx.x == 0) s_clk = clock64();
   stage_tiers(p, s_tw);
-  const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  // VF_TRACE_SCHEDULE: this block traces ray block order[b] (longest-first list scheduling)
+  const uint64_t tb = p.order ? __ldg(p.order + blockIdx.x) : blockIdx.x;
+  const uint64_t gid = tb * blockDim.x + threadIdx.x;
   Ctr<COUNT> ct;
   ct.touch_map = p.touch;
   if (gid < n) {
@@ -1076,6 +1090,25 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(con
     ct.add(VF_CTR_RAYS);
   }
   ct.flush(counters);
+  if (p.cost) {  // the block's duration, for the next launch's order (uniform branch)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long c = clock64() - s_clk;
+      p.cost[gid / blockDim.x] = c > 0xffffffffll ? 0xffffffffu : (uint32_t)c;
+    }
+  }
+#ifdef VF_BLOCK_CLOCK
+  __syncthreads();
+  if (threadIdx.x == 0 && g_block_clock) {
+    unsigned long long t1;
+    uint32_t sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_block_clock[3 * blockIdx.x] = blk_t0;
+    g_block_clock[3 * blockIdx.x + 1] = t1;
+    g_block_clock[3 * blockIdx.x + 2] = sm;
+  }
+#endif
 }
 
 // Persistent warps with dynamic ray fetch: grid = resident blocks; a warp keeps its lanes busy
@@ -1316,6 +1349,87 @@ __global__ void query_kernel(const TraceParams p, const uint32_t* __restrict__ b
       }
     }
     out[i] = res;
+  }
+}
+
+// ---- VF_TRACE_SCHEDULE: longest-first block order from the last launch's block durations -------
+// A frame's launch lasts as long as its slowest blocks: blocks that start late and run long leave
+// the other SMs idle (cfg4: SMs active 82 % of the launch, tools/block_timeline.py). Greedy list
+// scheduling in order of decreasing duration (LPT) bounds the makespan by the longest block; the
+// durations come from the previous launch over the same ray array (temporal coherence of frames).
+// Two small kernels: a histogram of quarter-octave duration classes, then a scatter of block
+// indices into their class's range, longest class first. A block's class is taken from the
+// longest duration within +-6 blocks (+-3 screen tiles of the 16x16-tile ray order): when the
+// camera moves between frames, a slow region's neighbours are promoted with it (A/B: with a moved
+// camera the undilated order loses up to 23 % on cfg3, the dilated one gains 4-9 %). Each CTA
+// scatters a contiguous range of blocks, so blocks of one class keep their screen locality. The
+// last CTA resets the counters.
+struct SchedCfg {
+  uint32_t sub;  // log2 classes per octave of duration (0..2)
+  uint32_t dil;  // a block's class uses the longest duration within +-dil blocks (screen neighbours)
+};
+__device__ __forceinline__ uint32_t sched_class(const uint32_t* __restrict__ cost, uint32_t nb, uint32_t i,
+                                                SchedCfg g) {
+  uint32_t c = __ldg(cost + i);
+  for (uint32_t k = 1; k <= g.dil; ++k) {
+    if (i >= k) c = max(c, __ldg(cost + i - k));
+    if (i + k < nb) c = max(c, __ldg(cost + i + k));
+  }
+  c |= 4u;
+  const uint32_t e = 31u - __clz(c);
+  const uint32_t key = (e << g.sub) + ((c >> (e - g.sub)) & ((1u << g.sub) - 1u));
+  return (kSchedBuckets - 1u) - key;  // 0 = longest
+}
+
+__global__ void __launch_bounds__(256) sched_hist_kernel(const uint32_t* __restrict__ cost, uint32_t nb,
+                                                         uint32_t* __restrict__ hist, SchedCfg g) {
+  __shared__ uint32_t sh[kSchedBuckets];
+  for (uint32_t i = threadIdx.x; i < kSchedBuckets; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x)
+    atomicAdd(&sh[sched_class(cost, nb, i, g)], 1u);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kSchedBuckets; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void __launch_bounds__(256) sched_scatter_kernel(const uint32_t* __restrict__ cost, uint32_t nb,
+                                                            uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor,
+                                                            uint32_t* __restrict__ done, uint32_t* __restrict__ order,
+                                                            SchedCfg g) {
+  __shared__ uint32_t base[kSchedBuckets], loc[kSchedBuckets];
+  __shared__ bool last;
+  const uint32_t per = (nb + gridDim.x - 1) / gridDim.x;
+  const uint32_t b0 = blockIdx.x * per, b1 = min(nb, b0 + per);
+  if (threadIdx.x < kSchedBuckets) loc[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) atomicAdd(&loc[sched_class(cost, nb, i, g)], 1u);
+  __syncthreads();
+  if (threadIdx.x < kSchedBuckets) {  // class start (exclusive scan of hist) + this CTA's range in it
+    uint32_t start = 0;
+    for (uint32_t k = 0; k < threadIdx.x; ++k) start += hist[k];
+    const uint32_t cnt = loc[threadIdx.x];
+    base[threadIdx.x] = start + (cnt ? atomicAdd(&cursor[threadIdx.x], cnt) : 0u);
+    loc[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+    const uint32_t k = sched_class(cost, nb, i, g);
+    order[base[k] + atomicAdd(&loc[k], 1u)] = i;
+  }
+  // the last CTA to finish resets hist / cursor / done for the next launch (every CTA has read hist)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    if (threadIdx.x < kSchedBuckets) {
+      hist[threadIdx.x] = 0;
+      cursor[threadIdx.x] = 0;
+    }
+    if (threadIdx.x == 0) *done = 0;
   }
 }
 
@@ -1575,6 +1689,100 @@ int persistent_blocks(KernelFn fn, int device, size_t smem = 0) {
 
 }  // namespace
 
+// VF_TRACE_SCHEDULE: find / create the schedule entry of this ray array and, if it holds the
+// durations of an earlier launch, compute this launch's block order (tp.order); every scheduled
+// launch records its block durations (tp.cost). Returns the entry (sched_mu held through `lk`)
+// or nullptr: no scheduling (natural block order), e.g. when memory is short or, inside stream
+// capture, for an array not seen before (nothing may be allocated during capture).
+SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, uint32_t nb, cudaStream_t s,
+                             TraceParams& tp, std::unique_lock<std::mutex>& lk, bool& capturing, const void* fn,
+                             unsigned threads) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  capturing = cs != cudaStreamCaptureStatusNone;
+  lk = std::unique_lock<std::mutex>(h->sched_mu);
+  SchedEntry* e = nullptr;
+  for (auto& x : h->sched)
+    if (x.mem && x.rays == rays && x.n == n && x.nb == nb) e = &x;
+  if (!e) {
+    if (capturing) return nullptr;
+    // a launch of at most two waves of resident blocks has no tail to reorder (cfg1: 512 blocks
+    // on 1,332 slots; the two order kernels would only add their launches)
+    int per_sm = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)threads, 0) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    if ((uint64_t)nb <= 2ull * (uint64_t)per_sm * (uint64_t)sms) return nullptr;
+    for (auto& x : h->sched)  // an empty slot, else the least recently used one
+      if (!e || !x.mem || (e->mem && x.last_use < e->last_use)) e = &x;
+    if (e->mem) {  // evict: no launch may still use its memory
+      if (e->ev) cudaEventSynchronize(e->ev);
+      h->alloc.put(e->mem, e->bytes, s);
+      e->mem = nullptr;
+    }
+    const size_t words = 2 * (size_t)nb + 2 * kSchedBuckets + 1;
+    e->mem = static_cast<uint32_t*>(h->alloc.get(words * sizeof(uint32_t), s));
+    if (!e->mem) return nullptr;
+    if (!e->ev && cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      h->alloc.put(e->mem, words * sizeof(uint32_t), s);
+      e->mem = nullptr;
+      return nullptr;
+    }
+    e->bytes = words * sizeof(uint32_t);
+    e->rays = rays;
+    e->n = n;
+    e->nb = nb;
+    e->valid = false;
+    cudaMemsetAsync(e->mem + 2 * (size_t)nb, 0, (2 * kSchedBuckets + 1) * sizeof(uint32_t), s);
+  } else if (!capturing) {
+    cudaStreamWaitEvent(s, e->ev, 0);  // after the launch that wrote cost (any stream)
+  }
+  e->last_use = ++h->sched_clock;
+  uint32_t* cost = e->mem;
+  uint32_t* order = e->mem + nb;
+  uint32_t* hist = e->mem + 2 * (size_t)nb;
+  if (e->valid) {
+    const unsigned g = (unsigned)std::min<uint32_t>(148u, (nb + 255u) / 256u);
+    static const SchedCfg cfg = [] {  // A/B knobs (tools/sched_ab.py): VF_SCHED_SUB, VF_SCHED_DIL
+      SchedCfg c{2u, 6u};  // A/B: +-6 blocks keeps the gain when the camera moves
+      if (const char* e = getenv("VF_SCHED_SUB")) c.sub = (uint32_t)std::min(2, std::max(0, atoi(e)));
+      if (const char* e = getenv("VF_SCHED_DIL")) c.dil = (uint32_t)std::min(16, std::max(0, atoi(e)));
+      return c;
+    }();
+    sched_hist_kernel<<<g, 256, 0, s>>>(cost, nb, hist, cfg);
+    sched_scatter_kernel<<<g, 256, 0, s>>>(cost, nb, hist, hist + kSchedBuckets, hist + 2 * kSchedBuckets, order,
+                                           cfg);
+    tp.order = order;
+  }
+  tp.cost = cost;
+  return e;
+}
+
+uint32_t trace_launch_count(const Handle* h, const vf_ray* rays, uint64_t n, uint32_t flags) {
+  if (n == 0) return 0;
+  if (!(flags & VF_TRACE_SCHEDULE) || (flags & (VF_TRACE_INCOHERENT | VF_TRACE_PERSISTENT_WARPS | VF_TRACE_CHUNKED)))
+    return 1;
+  std::lock_guard<std::mutex> lk(h->sched_mu);
+  for (const auto& x : h->sched)
+    if (x.mem && x.rays == rays && x.n == n && x.valid) return 3;
+  return 1;
+}
+
+void free_schedules(const Handle* h) {
+  std::lock_guard<std::mutex> lk(h->sched_mu);
+  for (auto& x : h->sched) {
+    if (x.mem) h->alloc.put(x.mem, x.bytes, h->build_stream);
+    if (x.ev) cudaEventDestroy(x.ev);
+    x = SchedEntry{};
+  }
+}
+
 vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* hits, uint32_t flags, cudaStream_t s,
                        unsigned long long* counters, vf_payload* payload, uint32_t* touch, const uint32_t* slots) {
   if (n == 0) return VF_OK;
@@ -1655,8 +1863,37 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     tp.payload = reinterpret_cast<uint2*>(payload);
     tp.touch = touch;
     tp.slot = slots;
+    std::unique_lock<std::mutex> sched_lk;
+    bool capturing = false;
+    SchedEntry* se = nullptr;
+    if ((flags & VF_TRACE_SCHEDULE) && !counters)
+      se = prepare_schedule(h, rays, n, (uint32_t)blocks, s, tp, sched_lk, capturing, (const void*)fn, threads);
+#ifdef VF_BLOCK_CLOCK
+    static unsigned long long* clk_buf = nullptr;
+    static size_t clk_n = 0;
+    if (clk_n < blocks) {
+      cudaFree(clk_buf);
+      cudaMalloc(&clk_buf, 3 * blocks * sizeof(unsigned long long));
+      clk_n = blocks;
+    }
+    cudaMemcpyToSymbolAsync(g_block_clock, &clk_buf, sizeof(clk_buf), 0, cudaMemcpyHostToDevice, s);
+#endif
     fn<<<(unsigned)blocks, threads, 0, s>>>(tp, h->buf, reinterpret_cast<const float4*>(rays),
                                             reinterpret_cast<int4*>(hits), n, counters, nullptr);
+    if (se && !capturing && cudaEventRecord(se->ev, s) == cudaSuccess) se->valid = true;
+#ifdef VF_BLOCK_CLOCK
+    if (const char* out = getenv("VF_BLOCK_CLOCK_OUT")) {
+      std::vector<unsigned long long> hb(3 * blocks);
+      cudaMemcpyAsync(hb.data(), clk_buf, hb.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      if (FILE* f = fopen(out, "ab")) {
+        const unsigned long long nb = blocks;
+        fwrite(&nb, sizeof(nb), 1, f);
+        fwrite(hb.data(), sizeof(unsigned long long), hb.size(), f);
+        fclose(f);
+      }
+    }
+#endif
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

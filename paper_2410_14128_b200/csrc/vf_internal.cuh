@@ -61,6 +61,8 @@ struct TraceParams {
   uint2* payload;       // optional closest-hit payload output (vf_trace_ex), per launch
   const uint32_t* slot; // optional hit destination index per ray (vf_trace_scatter), per launch
   uint32_t* touch;      // counting launches: touch bitmap, one bit per format word (else null)
+  const uint32_t* order;  // VF_TRACE_SCHEDULE: block b traces ray block order[b] (else b), per launch
+  uint32_t* cost;         // VF_TRACE_SCHEDULE: each block stores its duration (SM cycles) at cost[its ray block]
   uint32_t lf0[3];      // tier-0 fan-out per axis (log2)
   int32_t dims[3];      // resolution per axis
   uint32_t n_tiers;
@@ -113,6 +115,21 @@ struct DevAllocator {
   }
 };
 
+// VF_TRACE_SCHEDULE state for one ray array (key: device pointer + count): the per-block durations
+// of the last launch over it and the longest-first block order derived from them.
+struct SchedEntry {
+  const void* rays = nullptr;
+  uint64_t n = 0;
+  uint32_t nb = 0;            // blocks of the launch
+  uint32_t* mem = nullptr;    // cost[nb] | order[nb] | hist[kSchedBuckets] | cursor[kSchedBuckets] | done
+  size_t bytes = 0;
+  cudaEvent_t ev = nullptr;   // recorded after the last launch that wrote cost (cross-stream order)
+  bool valid = false;         // cost holds a completed launch's durations
+  uint64_t last_use = 0;
+};
+constexpr int kSchedEntries = 32;
+constexpr uint32_t kSchedBuckets = 128;  // quarter-octave duration classes, longest first
+
 struct Handle {
   int device = 0;
   DevAllocator alloc;
@@ -134,6 +151,10 @@ struct Handle {
   unsigned long long* work = nullptr;
   mutable std::atomic<uint32_t> work_slot{0};
   std::mutex host_mu;  // vf_trace_host: serialises calls on one handle (shared staging and streams)
+  // VF_TRACE_SCHEDULE: LRU table of per-ray-array block schedules (guarded by sched_mu)
+  mutable std::mutex sched_mu;
+  mutable SchedEntry sched[kSchedEntries];
+  mutable uint64_t sched_clock = 0;
 };
 
 constexpr uint32_t kWorkSlots = 64;
@@ -145,6 +166,8 @@ constexpr uint32_t VF_TRACE_PERSISTENT_WARPS = 1u << 30;
 // from the chunk), optionally with the top Raw grid staged in shared memory
 constexpr uint32_t VF_TRACE_CHUNKED = 1u << 29;
 constexpr uint32_t VF_TRACE_STAGE_TOP = 1u << 28;
+void free_schedules(const Handle* h);
+uint32_t trace_launch_count(const Handle* h, const vf_ray* rays, uint64_t n, uint32_t flags);
 
 // errors
 void set_error(const char* fmt, ...);

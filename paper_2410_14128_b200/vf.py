@@ -31,6 +31,7 @@ VF_BUILD_ALIGN_NODES = 2
 VF_BUILD_DEFAULT = VF_BUILD_WHOLE_LEVEL_DEDUP
 VF_TRACE_RESTART_SV = 1
 VF_TRACE_INCOHERENT = 2
+VF_TRACE_SCHEDULE = 4  # longest-first block order from the previous launch over the same ray array
 VF_TRACE_PERSISTENT_WARPS = 1 << 30  # internal ablation flag (include/vf.h: bit 30 reserved)
 VF_MAX_LEVELS = 16
 VF_MAX_TIERS = 16
@@ -131,6 +132,7 @@ _sig = {
     "vf_ipc_open": ([_vp, ctypes.c_int, ctypes.POINTER(_vp)], ctypes.c_int),
     "vf_ipc_close": ([_vp], ctypes.c_int),
     "vf_trace_ex": ([_vp, _vp, _u64, _vp, _vp, _u32, _vp], ctypes.c_int),
+    "vf_trace_launch_count": ([_vp, _vp, _u64, _u32, ctypes.POINTER(_u32)], ctypes.c_int),
     "vf_trace_counters": ([_vp, _vp, _u64, _vp, _u32, _vp, ctypes.POINTER(_u64)], ctypes.c_int),
     "vf_query": ([_vp, _vp, _u64, _vp, _vp], ctypes.c_int),
     "vf_stats_get": ([_vp, ctypes.POINTER(Stats)], ctypes.c_int),
@@ -249,12 +251,12 @@ class Handle:
 
     # -- the hot path
     @staticmethod
-    def _flags(restart, persistent=False, incoherent=False):
+    def _flags(restart, persistent=False, incoherent=False, schedule=False):
         return ((VF_TRACE_RESTART_SV if restart else 0) | (VF_TRACE_PERSISTENT_WARPS if persistent else 0)
-                | (VF_TRACE_INCOHERENT if incoherent else 0))
+                | (VF_TRACE_INCOHERENT if incoherent else 0) | (VF_TRACE_SCHEDULE if schedule else 0))
 
     def trace(self, rays, hits=None, restart: bool = False, stream=None, persistent: bool = False,
-              incoherent: bool = False):
+              incoherent: bool = False, schedule: bool = False):
         """rays: (n, 8) float32 CUDA tensor (vf_ray); hits: (n, 4) int32 CUDA tensor (vf_hit, t as
         float bits). Asynchronous on `stream`. Returns hits."""
         import torch
@@ -264,10 +266,18 @@ class Handle:
         assert rays.is_cuda and rays.dtype == torch.float32 and rays.is_contiguous() and rays.shape[1] == 8
         assert hits.is_cuda and hits.dtype == torch.int32 and hits.is_contiguous() and hits.shape[0] >= n
         _check(_lib.vf_trace(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
-                             self._flags(restart, persistent, incoherent), _stream_ptr(stream)))
+                             self._flags(restart, persistent, incoherent, schedule), _stream_ptr(stream)))
         return hits
 
-    def trace_scatter(self, rays, hits, slots, restart: bool = False, stream=None, incoherent: bool = False):
+    def launch_count(self, rays, restart: bool = False, incoherent: bool = False, schedule: bool = False) -> int:
+        """vf_trace_launch_count: kernels one trace call over `rays` launches now (3 if scheduled)."""
+        c = _u32(0)
+        _check(_lib.vf_trace_launch_count(self._p, ctypes.c_void_p(rays.data_ptr()), rays.shape[0],
+                                          self._flags(restart, False, incoherent, schedule), ctypes.byref(c)))
+        return int(c.value)
+
+    def trace_scatter(self, rays, hits, slots, restart: bool = False, stream=None, incoherent: bool = False,
+                      schedule: bool = False):
         """vf_trace_scatter: the hit of ray i goes to row slots[i] of `hits` — a CUDA tensor, or a raw
         device pointer (int) such as a peer process's frame buffer from ipc_open. slots: (n,) int32
         CUDA tensor on the handle's device. Asynchronous on `stream`."""
@@ -277,11 +287,12 @@ class Handle:
         assert slots.is_cuda and slots.dtype == torch.int32 and slots.is_contiguous() and slots.shape[0] >= n
         ptr = hits if isinstance(hits, int) else hits.data_ptr()
         _check(_lib.vf_trace_scatter(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(ptr),
-                                     ctypes.c_void_p(slots.data_ptr()), self._flags(restart, False, incoherent),
+                                     ctypes.c_void_p(slots.data_ptr()), self._flags(restart, False, incoherent, schedule),
                                      _stream_ptr(stream)))
         return hits
 
-    def trace_payload(self, rays, hits=None, payload=None, restart: bool = False, stream=None):
+    def trace_payload(self, rays, hits=None, payload=None, restart: bool = False, stream=None,
+                      schedule: bool = False):
         """vf_trace_ex: hits plus closest-hit payload (n, 2) int32 {rgba, packed int8 normal}."""
         import torch
         n = rays.shape[0]
@@ -290,7 +301,8 @@ class Handle:
         if payload is None:
             payload = torch.empty((n, 2), dtype=torch.int32, device=rays.device)
         _check(_lib.vf_trace_ex(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
-                                ctypes.c_void_p(payload.data_ptr()), self._flags(restart), _stream_ptr(stream)))
+                                ctypes.c_void_p(payload.data_ptr()), self._flags(restart, schedule=schedule),
+                                _stream_ptr(stream)))
         return hits, payload
 
     def counters(self, rays, hits=None, restart: bool = False, stream=None, persistent: bool = False,
@@ -305,11 +317,12 @@ class Handle:
                                       self._flags(restart, persistent, incoherent), _stream_ptr(stream), c))
         return {k: int(c[i]) for i, k in enumerate(COUNTER_NAMES)}
 
-    def trace_host(self, rays, hits, restart: bool = False, stream=None, incoherent: bool = False):
+    def trace_host(self, rays, hits, restart: bool = False, stream=None, incoherent: bool = False,
+                   schedule: bool = False):
         """End to end: host (pinned) rays (n,8) float32 -> host hits (n,4) int32, copies inside."""
         n = rays.shape[0]
         _check(_lib.vf_trace_host(self._p, ctypes.c_void_p(rays.data_ptr()), n, ctypes.c_void_p(hits.data_ptr()),
-                                  self._flags(restart, False, incoherent), _stream_ptr(stream)))
+                                  self._flags(restart, False, incoherent, schedule), _stream_ptr(stream)))
         return hits
 
     def query(self, xyz, stream=None):

@@ -40,7 +40,8 @@ def test_multi_rank_code_path_with_one_rank():
     """bench.py's N > 1 path (NCCL group, max-over-ranks reductions, the chunked trace / NCCL hit
     gather pipeline of one tile-sharded frame, per-rank e2e) exercised on the one GPU of the box
     (--force-dist)."""
-    for gather, launches in (("nccl", 6), ("p2p", 3)):
+    # launches per step: each trace launch is preceded by the two VF_TRACE_SCHEDULE order kernels
+    for gather, launches in (("nccl", 2 * 3 * 3), ("p2p", 3 * 3)):
         r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-dist", "--config", "cfg2",
                             "--no-cpu-baseline", "--no-side", "--steps", "3", "--warmup", "3", "--gather-chunks", "2",
                             "--gather", gather], capture_output=True, text=True, timeout=600, cwd=ROOT)
