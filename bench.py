@@ -469,6 +469,10 @@ def run_ours(args):
     else:
         own = np.arange(n_total)
         counts = [n_total]
+    replicas = None
+    if dist_on:  # §8(e) "Replicas": every rank built the same volume; compare digests over gloo
+        gloo = dist.new_group(backend="gloo")
+        replicas = shard.verify_replicas(shard.replica_digest(handle), group=gloo)
     rays = torch.from_numpy(np.ascontiguousarray(rays_all[own])).to(dev)
     stream = torch.cuda.current_stream()
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
@@ -569,6 +573,8 @@ def run_ours(args):
             issue = {"bound": "issue", "frac": round(ach_i / peak_i, 3), "unit": "warp-inst/s",
                      "warp_inst_per_ray": round(ent["warp_inst_per_launch"] / ent_rays, 1),
                      "threads_per_warp_inst": round(ent.get("thread_inst_per_launch", 0) / ent["warp_inst_per_launch"], 1)}
+        launches_step = step.launches_per_step(
+            lambda v: handle.launch_count(v, restart=args.restart, incoherent=incoh, schedule=sched))
         hits_np = step.local_hits().cpu().numpy()
         gxyz, gt = hits_np[:, :3], hits_np[:, 3].view(np.float32)
         cpu = None
@@ -588,17 +594,19 @@ def run_ours(args):
                        "hit_rate": round(float((gxyz[:, 0] >= 0).mean()), 4), "build_s": round(build_s, 3),
                        "voxel_gen_s": round(gen_s, 2), "l2": "flushed between timed steps (2x126 MB write)",
                        "schedule": ("longest-first block order from the previous frame's per-block durations "
-                                    "(VF_TRACE_SCHEDULE; same camera every frame)") if sched else "index order",
+                                    "(VF_TRACE_SCHEDULE; same camera every frame)") if launches_step > step.launches
+                       else "index order" + (" (a launch of <= 2 waves: nothing to reorder)" if sched else ""),
                        "parallelism": f"tile{world}: one frame's 16x16 tiles interleaved over {world} GPU(s), volume "
                                       f"replicated" + (
                                           ", fused trace + hit scatter into rank 0's frame over peer memory (CUDA IPC)"
                                           if step.gather == "p2p" else
                                           f", NCCL gather of hits to rank 0 in {step.launches} chunks"
-                                          if dist_on else "") + (f" [{step.gather_note}]" if step.gather_note else "")},
+                                          if dist_on else "") + (f" [{step.gather_note}]" if step.gather_note else "") + (
+                                          f"; replicas verified on {replicas} rank(s) (bytes_used, buffer and "
+                                          f"vf_query digests over gloo)" if replicas else "")},
             "e2e": {"value": round(e2e_val, 1), "unit": "Mrays/s", "h2d_bytes_per_step": n_total * 32,
                     "d2h_bytes_per_step": n_total * 16},
-            "gpu_launches": args.steps * step.launches_per_step(
-                lambda v: handle.launch_count(v, restart=args.restart, incoherent=incoh, schedule=sched)),
+            "gpu_launches": args.steps * launches_step,
             "roofline": roof, "issue_roofline": issue, "cpu_baseline": cpu, "clocks": clk,
             "trace_only": round(n_total / (kern_max / 1e3) / 1e6, 1),
         }

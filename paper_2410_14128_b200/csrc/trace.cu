@@ -1055,12 +1055,16 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(con
                                                     uint64_t n, unsigned long long* __restrict__ counters,
                                                     unsigned long long* __restrict__ work) {
   __shared__ __align__(16) uint32_t s_tw[8 * VF_MAX_TIERS];
-  __shared__ long long s_clk;  // VF_TRACE_SCHEDULE: the block's start (SM cycles)
+  __shared__ long long s_clk;      // VF_TRACE_SCHEDULE: the block's start (SM cycles)
+  __shared__ uint32_t s_warps_done;  // ... and its finished warps
 #ifdef VF_BLOCK_CLOCK  // analysis build (tools/block_timeline.py): per-block start / end / SM
   unsigned long long blk_t0 = 0;
   if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(blk_t0));
 #endif
-  if (p.cost && threadIdx.x == 0) s_clk = clock64();
+  if (p.cost && threadIdx.x == 0) {  // (ordered before every read by stage_tiers' barrier)
+    s_clk = clock64();
+    s_warps_done = 0;
+  }
   stage_tiers(p, s_tw);
   // VF_TRACE_SCHEDULE: this block traces ray block order[b] (longest-first list scheduling)
   const uint64_t tb = p.order ? __ldg(p.order + blockIdx.x) : blockIdx.x;
@@ -1090,11 +1094,11 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(con
     ct.add(VF_CTR_RAYS);
   }
   ct.flush(counters);
-  if (p.cost) {  // the block's duration, for the next launch's order (uniform branch)
-    __syncthreads();
-    if (threadIdx.x == 0) {
+  if (p.cost) {  // the block's duration, for the next launch's order (uniform branch): the last
+    __syncwarp();  // warp to finish stores it (no block barrier: finished warps exit)
+    if ((threadIdx.x & 31u) == 0 && atomicAdd(&s_warps_done, 1u) == blockDim.x / 32u - 1u) {
       const long long c = clock64() - s_clk;
-      p.cost[gid / blockDim.x] = c > 0xffffffffll ? 0xffffffffu : (uint32_t)c;
+      p.cost[gid / blockDim.x] = c > 0xffffffffll ? 0xffffffffu : (uint32_t)c;  // = tb
     }
   }
 #ifdef VF_BLOCK_CLOCK

@@ -29,6 +29,43 @@ def shard_counts(perm: np.ndarray, width: int, world: int, tile: int = TILE):
     return [int((t == r).sum()) for r in range(world)]
 
 
+def replica_digest(handle, slabs: int = 8, step: int = 16) -> dict:
+    """Digest of this rank's replica of the volume (SURVEY.md §8(e) "Replicas": every rank builds the
+    format from the same descriptor and seed; the build is deterministic): bytes_used, the
+    non-empty voxel count, a position-weighted checksum of the format buffer's words, and a
+    checksum of vf_query over `slabs` z-slabs sampled every `step` voxels in x and y (the voxels
+    the format answers for, through the library's own lookup). Host integers only."""
+    import torch
+    st = handle.stats()
+    words = handle.buffer_words().astype(np.uint64)
+    wsum = int(np.sum(words * (2 * np.arange(words.size, dtype=np.uint64) + 1), dtype=np.uint64))
+    rx, ry, rz = st["dims"]
+    xs, ys = np.arange(0, rx, step), np.arange(0, ry, step)
+    gx, gy = np.meshgrid(xs, ys, indexing="ij")
+    qsum = 0
+    for k in range(slabs):
+        z = (2 * k + 1) * rz // (2 * slabs)
+        xyz = np.stack([gx.ravel(), gy.ravel(), np.full(gx.size, z)], 1).astype(np.int32)
+        rgba = handle.query(torch.from_numpy(xyz).cuda()).cpu().numpy().astype(np.uint32).astype(np.uint64)
+        qsum = (qsum * 1000003 + int(np.sum(rgba * (2 * np.arange(rgba.size, dtype=np.uint64) + 1),
+                                            dtype=np.uint64))) % (1 << 64)
+    return {"bytes_used": int(st["bytes_used"]), "nonempty_voxels": int(st["nonempty_voxels"]),
+            "buffer_checksum": wsum, "query_checksum": qsum, "query_samples": int(slabs * gx.size)}
+
+
+def verify_replicas(digest: dict, group=None) -> int:
+    """Compare every rank's replica_digest over `group` (a gloo group: host objects, no NCCL);
+    raises on every rank if any two differ. Returns the number of ranks compared."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    got = [None] * world
+    dist.all_gather_object(got, digest, group=group)
+    bad = [r for r, d in enumerate(got) if d != got[0]]
+    if bad:
+        raise RuntimeError(f"volume replicas differ: rank 0 {got[0]} vs rank(s) {bad}: {[got[r] for r in bad]}")
+    return world
+
+
 def gather_hits(hits, counts, group=None, dst: int = 0):
     """Gather every rank's (n_r, 4) int32 hit buffer to `dst` (one collective). Returns the list
     of per-rank buffers on dst, None elsewhere."""

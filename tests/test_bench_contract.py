@@ -50,6 +50,7 @@ def test_multi_rank_code_path_with_one_rank():
         assert d["value"] > 0 and d["scaling"] == "strong" and d["gpu_launches"] == launches and d["e2e"]["value"] > 0
         assert d["trace_only"] >= 0.9 * d["value"]
         assert ("peer memory" in d["config"]["parallelism"]) == (gather == "p2p"), d["config"]["parallelism"]
+        assert "replicas verified on 1 rank" in d["config"]["parallelism"], d["config"]["parallelism"]
 
 
 @pytest.mark.gpu

@@ -308,3 +308,60 @@ def test_peer_frame_protocol_gloo(fail_rank):
         assert got[1] == ("ok", 0x1001, [1, 2, 3], False)
     else:
         assert all(r[0] == "failed" and "no peer access" in r[1] for r in got.values()), got
+
+
+def _replica_worker(rank, world, port, differ, q):
+    import torch.distributed as dist
+    from paper_2410_14128_b200 import shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    d = {"bytes_used": 1000, "nonempty_voxels": 10, "buffer_checksum": 12345, "query_checksum": 678,
+         "query_samples": 64}
+    if differ and rank == 1:
+        d["buffer_checksum"] += 1
+    try:
+        q.put((rank, ("ok", shard.verify_replicas(d))))
+    except RuntimeError as e:
+        q.put((rank, ("differ", str(e))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("differ", [False, True])
+def test_replica_verification_gloo(differ):
+    """SURVEY §8(e) "Replicas": the ranks' volume digests are compared over gloo; a mismatch on any
+    rank raises on every rank."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replica_worker, args=(r, world, port, differ, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    if differ:
+        assert all(v[0] == "differ" and "replicas differ" in v[1] for v in got.values()), got
+    else:
+        assert got == {0: ("ok", 2), 1: ("ok", 2)}
+
+
+@pytest.mark.gpu
+def test_replica_digest_is_deterministic_and_discriminating():
+    """Two builds of the same volume and format have equal digests (the replicas of a multi-GPU run);
+    a different volume does not."""
+    import inputs
+    from paper_2410_14128_b200 import shard, vf
+    d1, d2 = inputs.menger(128, 4), inputs.menger(128, 3)
+    digests = []
+    for d in (d1, d1, d2):
+        keys, rgba = inputs.voxels_device(d)
+        h = vf.build((keys, rgba, (128, 128, 128)), "R(3, 3, 3) G(4)")
+        digests.append(shard.replica_digest(h, slabs=4, step=4))
+        h.close()
+    assert digests[0] == digests[1]
+    assert digests[0]["query_checksum"] != digests[2]["query_checksum"]
+    assert digests[0]["buffer_checksum"] != digests[2]["buffer_checksum"]
+    assert digests[0]["query_samples"] == 4 * 32 * 32
