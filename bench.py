@@ -396,7 +396,7 @@ def side_cfg4(args, stream, flush):
     rays_np, _ = make_rays("cfg4")
     rays = torch.from_numpy(np.ascontiguousarray(rays_np)).cuda()
     hits = torch.empty((rays.shape[0], 4), dtype=torch.int32, device="cuda")
-    sched = args.schedule == "on"
+    sched = {"on": True, "off": False, "regroup": "regroup"}[args.schedule]
 
     def timed(schedule):
         for _ in range(3):
@@ -478,7 +478,9 @@ def run_ours(args):
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
     incoh = CONFIGS[cfg][1] == "incoherent"  # VF_TRACE_INCOHERENT hint (not for cfg4s: its screen-ordered secondary rays are coherent enough, plain kernel +36 %)
 
-    sched = args.schedule == "on" and not incoh  # VF_TRACE_SCHEDULE (coherent launches only)
+    sched = args.schedule != "off" and not incoh  # VF_TRACE_SCHEDULE (coherent launches only)
+    if sched and args.schedule == "regroup":
+        sched = "regroup"  # + VF_TRACE_REGROUP (opt-in: pays only when the camera does not move)
 
     def trace(rv, hv):
         handle.trace(rv, hv, restart=args.restart, incoherent=incoh, schedule=sched)
@@ -594,7 +596,9 @@ def run_ours(args):
                        "hit_rate": round(float((gxyz[:, 0] >= 0).mean()), 4), "build_s": round(build_s, 3),
                        "voxel_gen_s": round(gen_s, 2), "l2": "flushed between timed steps (2x126 MB write)",
                        "schedule": ("longest-first block order from the previous frame's per-block durations "
-                                    "(VF_TRACE_SCHEDULE; same camera every frame)") if launches_step > step.launches
+                                    "(VF_TRACE_SCHEDULE; same camera every frame)" + (
+                                        " + rays regrouped into warps by their iteration counts (VF_TRACE_REGROUP)"
+                                        if sched == "regroup" else "")) if launches_step > step.launches
                        else "index order" + (" (a launch of <= 2 waves: nothing to reorder)" if sched else ""),
                        "parallelism": f"tile{world}: one frame's 16x16 tiles interleaved over {world} GPU(s), volume "
                                       f"replicated" + (
@@ -783,8 +787,9 @@ def main(argv=None):
     ap.add_argument("--gather-chunks", type=int, default=0, help="N>1 nccl gather: trace/gather pipeline depth (0: auto)")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="N>1: fused trace + peer-memory hit scatter (p2p) or trace + NCCL gather")
-    ap.add_argument("--schedule", default="on", choices=["on", "off"],
-                    help="VF_TRACE_SCHEDULE: blocks ordered by the previous frame's block durations")
+    ap.add_argument("--schedule", default="on", choices=["on", "off", "regroup"],
+                    help="VF_TRACE_SCHEDULE: blocks ordered by the previous frame's block durations "
+                         "(regroup: + VF_TRACE_REGROUP, rays regrouped into warps by their iteration counts)")
     ap.add_argument("--force-dist", action="store_true", help="test aid: the N>1 code path with one rank")
     argv = sys.argv[1:] if argv is None else argv
     args = ap.parse_args(argv)

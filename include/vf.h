@@ -192,12 +192,21 @@ enum {
                                    The first launch over an array runs in index order, and so does
                                    every launch of at most two waves of resident blocks (nothing to
                                    reorder). The handle
-                                   keeps 8 B per block for up to 32 arrays (least recently used
+                                   keeps 8 B per block + 8 B per ray for up to 32 arrays (least recently used
                                    evicted; allocated through the build's vf_allocator); launches
                                    sharing an array are ordered by an event (inside stream capture
                                    the graph orders them, and an array first seen during capture
                                    runs unscheduled). Coherent-ray launches only (not with
                                    VF_TRACE_INCOHERENT, whose persistent warps balance by design). */
+  VF_TRACE_REGROUP = 1u << 3,    /* with VF_TRACE_SCHEDULE: also regroup the rays into warps.
+                                   Inside every group of 256 consecutive rays (a 16x16 screen tile
+                                   of a tile-ordered ray stream) the rays are ordered by their
+                                   iteration counts in the previous launch over the array, longest
+                                   first, so the lanes of a warp end together. Pays when the rays
+                                   repeat (a static view: +5-8 % on top of the schedule), costs up
+                                   to 10 % when the camera moves between launches (the per-ray
+                                   counts no longer match and warps lose their 8x4-pixel shape).
+                                   Results are identical. */
   /* bit 30 is reserved (internal ablation: persistent warps with dynamic ray refill) */
 };
 
@@ -213,7 +222,7 @@ VF_API vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf
 
 /* Kernel launches one vf_trace / vf_trace_ex / vf_trace_scatter call with these arguments makes
  * now (host-side query, no GPU work): 3 when VF_TRACE_SCHEDULE will reorder it (the two order
- * kernels + the trace), else 1. For launch accounting (bench.py's gpu_launches). */
+ * kernels + the trace; 4 with VF_TRACE_REGROUP), else 1. For launch accounting (bench.py). */
 VF_API vf_status vf_trace_launch_count(const vf_handle* h, const vf_ray* rays, uint64_t n, uint32_t trace_flags,
                                        uint32_t* count);
 

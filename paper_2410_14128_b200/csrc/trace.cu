@@ -39,6 +39,7 @@
 
 #include <algorithm>
 #include <mutex>
+
 #include <type_traits>
 #include <vector>
 
@@ -1066,19 +1067,23 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(con
     s_warps_done = 0;
   }
   stage_tiers(p, s_tw);
-  // VF_TRACE_SCHEDULE: this block traces ray block order[b] (longest-first list scheduling)
+  // VF_TRACE_SCHEDULE: this block takes slot block order[b] (longest-first list scheduling), and
+  // slot v traces ray ray_perm[v] (rays regrouped into warps by duration inside groups of 256)
   const uint64_t tb = p.order ? __ldg(p.order + blockIdx.x) : blockIdx.x;
-  const uint64_t gid = tb * blockDim.x + threadIdx.x;
+  uint64_t gid = tb * blockDim.x + threadIdx.x;
+  if (p.ray_perm && gid < n) gid = __ldg(p.ray_perm + gid);
   Ctr<COUNT> ct;
   ct.touch_map = p.touch;
   if (gid < n) {
     Lane<KINDS, RESTART, COUNT, D, false, ALN> L;
     uint32_t stk[VF_MAX_TIERS];
     int4 out = miss_record();
+    uint32_t iters = 0;  // VF_TRACE_SCHEDULE: this ray's iterations (its lane's share of the warp)
     if (L.start(p, buf, s_tw, __ldg(rays + 2 * gid), __ldg(rays + 2 * gid + 1), ct)) {
       int res;
       do {
         res = L.iterate(p, buf, s_tw, stk, ct);
+        ++iters;
       } while (res == IT_CONTINUE);
       if (res == IT_HIT) {
         out = L.hit_record();
@@ -1091,6 +1096,7 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(con
     if (COUNT) hits[gid].x = (int)ct.v[VF_CTR_CELL_TESTS];
 #endif
     if (p.payload && out.x < 0) p.payload[gid] = make_uint2(0u, 0u);
+    if (p.ray_cost) p.ray_cost[gid] = iters;  // the next launch's regrouping key
     ct.add(VF_CTR_RAYS);
   }
   ct.flush(counters);
@@ -1098,7 +1104,7 @@ __global__ void __launch_bounds__(kTraceThreads, D::kMinBlocks) trace_kernel(con
     __syncwarp();  // warp to finish stores it (no block barrier: finished warps exit)
     if ((threadIdx.x & 31u) == 0 && atomicAdd(&s_warps_done, 1u) == blockDim.x / 32u - 1u) {
       const long long c = clock64() - s_clk;
-      p.cost[gid / blockDim.x] = c > 0xffffffffll ? 0xffffffffu : (uint32_t)c;  // = tb
+      p.cost[p.order ? __ldg(p.order + blockIdx.x) : blockIdx.x] = c > 0xffffffffll ? 0xffffffffu : (uint32_t)c;
     }
   }
 #ifdef VF_BLOCK_CLOCK
@@ -1437,6 +1443,53 @@ __global__ void __launch_bounds__(256) sched_scatter_kernel(const uint32_t* __re
   }
 }
 
+// VF_TRACE_REGROUP: rays regrouped into warps by their iteration counts in the last launch. A warp
+// lasts as long as its longest ray, so inside each group of kRayGroup consecutive rays (one 16x16
+// screen tile of the tile-ordered ray stream) the rays are ordered by their last iteration count,
+// longest first: slot g*256 + r traces the group's r-th longest ray. A warp's slots stay inside
+// one tile (coherent upper levels) while its lanes become homogeneous in length (counting-run
+// simulation: warp-iterations per ray cfg4 24.6 -> 19.6, cfg5 37.0 -> 31.8). One CTA per group, a
+// stable counting sort over 32 quarter-octave classes (>= 128 iterations share class 0): lanes of
+// a warp with the same class find each other with __match_any_sync, a block-wide exclusive scan
+// over (class, warp) gives every lane its slot. Slots past n (a ragged last group) sort last.
+__global__ void __launch_bounds__(kRayGroup) sched_raysort_kernel(const uint32_t* __restrict__ ray_cost, uint64_t n,
+                                                                  uint32_t* __restrict__ ray_perm) {
+  constexpr uint32_t kWarps = kRayGroup / 32u, kClasses = 32u;
+  static_assert(kClasses * kWarps == kRayGroup, "one (class, warp) counter per thread");
+  __shared__ uint32_t cnt[kClasses * kWarps];  // [class][warp], then its exclusive prefix
+  __shared__ uint32_t wsum[kWarps];
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  const uint64_t i = (uint64_t)blockIdx.x * kRayGroup + threadIdx.x;
+  cnt[threadIdx.x] = 0;
+  uint32_t k = kClasses - 1u;
+  if (i < n) {
+    const uint32_t v = (__ldg(ray_cost + i) + 1u) << 2;
+    const uint32_t e = 31u - __clz(v);
+    k = kClasses - 1u - min(4u * (e - 2u) + ((v >> (e - 2u)) & 3u), kClasses - 1u);
+  }
+  const uint32_t peers = __match_any_sync(0xffffffffu, k);
+  const uint32_t below = __popc(peers & ((1u << lane) - 1u));
+  __syncthreads();
+  if (below == 0) cnt[k * kWarps + w] = __popc(peers);
+  __syncthreads();
+  // exclusive scan of cnt in (class, warp) order: one entry per thread
+  const uint32_t x = cnt[threadIdx.x];
+  uint32_t incl = x;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  uint32_t off = 0;
+  for (uint32_t q = 0; q < w; ++q) off += wsum[q];
+  __syncthreads();
+  cnt[threadIdx.x] = off + incl - x;
+  __syncthreads();
+  if (i < n) ray_perm[(uint64_t)blockIdx.x * kRayGroup + cnt[k * kWarps + w] + below] = (uint32_t)i;
+}
+
 using KernelFn = void (*)(const TraceParams, const uint32_t*, const float4*, int4*, uint64_t, unsigned long long*,
                           unsigned long long*);
 
@@ -1700,7 +1753,7 @@ int persistent_blocks(KernelFn fn, int device, size_t smem = 0) {
 // capture, for an array not seen before (nothing may be allocated during capture).
 SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, uint32_t nb, cudaStream_t s,
                              TraceParams& tp, std::unique_lock<std::mutex>& lk, bool& capturing, const void* fn,
-                             unsigned threads) {
+                             unsigned threads, bool regroup) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
     cudaGetLastError();
@@ -1729,7 +1782,7 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
       h->alloc.put(e->mem, e->bytes, s);
       e->mem = nullptr;
     }
-    const size_t words = 2 * (size_t)nb + 2 * kSchedBuckets + 1;
+    const size_t words = 2 * (size_t)nb + 2 * kSchedBuckets + 1 + 2 * (size_t)n;
     e->mem = static_cast<uint32_t*>(h->alloc.get(words * sizeof(uint32_t), s));
     if (!e->mem) return nullptr;
     if (!e->ev && cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming) != cudaSuccess) {
@@ -1751,6 +1804,8 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
   uint32_t* cost = e->mem;
   uint32_t* order = e->mem + nb;
   uint32_t* hist = e->mem + 2 * (size_t)nb;
+  uint32_t* ray_cost = hist + 2 * kSchedBuckets + 1;
+  uint32_t* ray_perm = ray_cost + n;
   if (e->valid) {
     const unsigned g = (unsigned)std::min<uint32_t>(148u, (nb + 255u) / 256u);
     static const SchedCfg cfg = [] {  // A/B knobs (tools/sched_ab.py): VF_SCHED_SUB, VF_SCHED_DIL
@@ -1763,8 +1818,13 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
     sched_scatter_kernel<<<g, 256, 0, s>>>(cost, nb, hist, hist + kSchedBuckets, hist + 2 * kSchedBuckets, order,
                                            cfg);
     tp.order = order;
+    if (regroup) {
+      sched_raysort_kernel<<<(unsigned)((n + kRayGroup - 1) / kRayGroup), kRayGroup, 0, s>>>(ray_cost, n, ray_perm);
+      tp.ray_perm = ray_perm;
+    }
   }
   tp.cost = cost;
+  if (regroup) tp.ray_cost = ray_cost;
   return e;
 }
 
@@ -1774,7 +1834,7 @@ uint32_t trace_launch_count(const Handle* h, const vf_ray* rays, uint64_t n, uin
     return 1;
   std::lock_guard<std::mutex> lk(h->sched_mu);
   for (const auto& x : h->sched)
-    if (x.mem && x.rays == rays && x.n == n && x.valid) return 3;
+    if (x.mem && x.rays == rays && x.n == n && x.valid) return (flags & VF_TRACE_REGROUP) ? 4 : 3;
   return 1;
 }
 
@@ -1871,7 +1931,8 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     bool capturing = false;
     SchedEntry* se = nullptr;
     if ((flags & VF_TRACE_SCHEDULE) && !counters)
-      se = prepare_schedule(h, rays, n, (uint32_t)blocks, s, tp, sched_lk, capturing, (const void*)fn, threads);
+      se = prepare_schedule(h, rays, n, (uint32_t)blocks, s, tp, sched_lk, capturing, (const void*)fn, threads,
+                            (flags & VF_TRACE_REGROUP) != 0);
 #ifdef VF_BLOCK_CLOCK
     static unsigned long long* clk_buf = nullptr;
     static size_t clk_n = 0;

@@ -63,6 +63,9 @@ struct TraceParams {
   uint32_t* touch;      // counting launches: touch bitmap, one bit per format word (else null)
   const uint32_t* order;  // VF_TRACE_SCHEDULE: block b traces ray block order[b] (else b), per launch
   uint32_t* cost;         // VF_TRACE_SCHEDULE: each block stores its duration (SM cycles) at cost[its ray block]
+  const uint32_t* ray_perm;  // VF_TRACE_SCHEDULE: slot v of the launch traces ray ray_perm[v] (else v)
+  uint32_t* ray_cost;        // VF_TRACE_SCHEDULE: each ray stores when its lane finished (SM cycles
+                             // after its block's start) at ray_cost[ray]
   uint32_t lf0[3];      // tier-0 fan-out per axis (log2)
   int32_t dims[3];      // resolution per axis
   uint32_t n_tiers;
@@ -122,6 +125,7 @@ struct SchedEntry {
   uint64_t n = 0;
   uint32_t nb = 0;            // blocks of the launch
   uint32_t* mem = nullptr;    // cost[nb] | order[nb] | hist[kSchedBuckets] | cursor[kSchedBuckets] | done
+                              // | ray_cost[n] | ray_perm[n]
   size_t bytes = 0;
   cudaEvent_t ev = nullptr;   // recorded after the last launch that wrote cost (cross-stream order)
   bool valid = false;         // cost holds a completed launch's durations
@@ -129,6 +133,7 @@ struct SchedEntry {
 };
 constexpr int kSchedEntries = 32;
 constexpr uint32_t kSchedBuckets = 128;  // quarter-octave duration classes, longest first
+constexpr uint32_t kRayGroup = 256;      // rays regrouped into warps inside consecutive groups of 256
 
 struct Handle {
   int device = 0;

@@ -32,6 +32,7 @@ VF_BUILD_DEFAULT = VF_BUILD_WHOLE_LEVEL_DEDUP
 VF_TRACE_RESTART_SV = 1
 VF_TRACE_INCOHERENT = 2
 VF_TRACE_SCHEDULE = 4  # longest-first block order from the previous launch over the same ray array
+VF_TRACE_REGROUP = 8   # with VF_TRACE_SCHEDULE: rays regrouped into warps by their last iteration counts
 VF_TRACE_PERSISTENT_WARPS = 1 << 30  # internal ablation flag (include/vf.h: bit 30 reserved)
 VF_MAX_LEVELS = 16
 VF_MAX_TIERS = 16
@@ -252,8 +253,10 @@ class Handle:
     # -- the hot path
     @staticmethod
     def _flags(restart, persistent=False, incoherent=False, schedule=False):
+        """schedule: False, True (VF_TRACE_SCHEDULE) or "regroup" (+ VF_TRACE_REGROUP)."""
         return ((VF_TRACE_RESTART_SV if restart else 0) | (VF_TRACE_PERSISTENT_WARPS if persistent else 0)
-                | (VF_TRACE_INCOHERENT if incoherent else 0) | (VF_TRACE_SCHEDULE if schedule else 0))
+                | (VF_TRACE_INCOHERENT if incoherent else 0) | (VF_TRACE_SCHEDULE if schedule else 0)
+                | (VF_TRACE_REGROUP if schedule == "regroup" else 0))
 
     def trace(self, rays, hits=None, restart: bool = False, stream=None, persistent: bool = False,
               incoherent: bool = False, schedule: bool = False):
@@ -270,7 +273,8 @@ class Handle:
         return hits
 
     def launch_count(self, rays, restart: bool = False, incoherent: bool = False, schedule: bool = False) -> int:
-        """vf_trace_launch_count: kernels one trace call over `rays` launches now (3 if scheduled)."""
+        """vf_trace_launch_count: kernels one trace call over `rays` launches now (3 if scheduled, 4
+        with regrouping)."""
         c = _u32(0)
         _check(_lib.vf_trace_launch_count(self._p, ctypes.c_void_p(rays.data_ptr()), rays.shape[0],
                                           self._flags(restart, False, incoherent, schedule), ctypes.byref(c)))

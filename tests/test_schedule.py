@@ -47,7 +47,8 @@ def test_schedule_state_allocated_only_for_multi_wave_launches():
     torch.cuda.synchronize()
     m2 = torch.cuda.memory_allocated()
     nb = (rays.shape[0] + 127) // 128
-    assert m2 - m1 >= hb.numel() * 4 + 8 * nb, (m2 - m1, hb.numel() * 4 + 8 * nb)
+    need = hb.numel() * 4 + 8 * nb + 8 * rays.shape[0]  # hits + per-block and per-ray schedule state
+    assert m2 - m1 >= need, (m2 - m1, need)
     _check(torch, hb, ref, "first scheduled launch")
     h.close()
 
@@ -58,13 +59,17 @@ def _check(torch, hits, ref, label):
     assert_parity(o[:, :3], o[:, 3].view(np.float32), ref, label)
 
 
-def test_scheduled_launches_equal_oracle():
+@pytest.mark.parametrize("mode", [True, "regroup"])
+def test_scheduled_launches_equal_oracle(mode):
+    """Block order (and with VF_TRACE_REGROUP the rays regrouped into warps inside 256-ray groups,
+    incl. the ragged last group) from the previous launch: every launch equals the oracle."""
     torch, vf, h, rays, ref = _setup()
     rt = torch.from_numpy(rays).cuda()
     for restart in (False, True):
-        for it in range(4):  # launch 0: index order; 1..3: ordered by the previous launch's durations
-            hits = h.trace(rt, restart=restart, schedule=True)
-            _check(torch, hits, ref, f"schedule launch {it} restart={restart}")
+        for it in range(4):  # launch 0: index order; 1..3: ordered by the previous launch
+            hits = h.trace(rt, restart=restart, schedule=mode)
+            _check(torch, hits, ref, f"schedule={mode} launch {it} restart={restart}")
+            assert h.launch_count(rt, restart=restart, schedule=mode) == (4 if mode == "regroup" else 3)
     h.close()
 
 
@@ -98,7 +103,7 @@ def test_schedule_inside_cuda_graph():
     torch.cuda.current_stream().wait_stream(s)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        h.trace(rt, hits, schedule=True, stream=torch.cuda.current_stream())
+        h.trace(rt, hits, schedule="regroup", stream=torch.cuda.current_stream())
     for it in range(3):
         hits.zero_()
         g.replay()

@@ -5,7 +5,7 @@ import sys, os, numpy as np, torch
 sys.path.insert(0, "/root/repo")
 import bench, inputs
 from paper_2410_14128_b200 import vf
-for cfg in ("cfg4", "cfg5", "cfg3", "cfg2"):
+for cfg in (sys.argv[1:] or ("cfg4", "cfg5", "cfg3", "cfg2")):
     vname, _, fmt, _ = bench.CONFIGS[cfg]
     vol = bench.make_volume(vname)
     k, c = inputs.voxels_device(vol)

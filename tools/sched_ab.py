@@ -48,19 +48,20 @@ for cfg in a.configs:
     ref = h.trace(rays).clone()
     res = {}
     for rep in range(2):
-        for mode in ("natural", "sched", "moved-0.005", "moved-0.05"):
+        for mode in ("natural", "sched", "regroup", "moved-0.005", "moved-0.005-regroup"):
             ms = []
             for i in range(a.reps + 3):
+                sm = "regroup" if mode.endswith("regroup") else mode != "natural"
                 if mode.startswith("moved"):
                     buf.copy_(prev[float(mode.split("-")[1])])
-                    h.trace(buf, hits, restart=a.restart, schedule=True)
+                    h.trace(buf, hits, restart=a.restart, schedule=sm)
                     buf.copy_(rays)
                 else:
                     buf.copy_(rays)
                 flush.fill_(i)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                h.trace(buf, hits, restart=a.restart, schedule=mode != "natural")
+                h.trace(buf, hits, restart=a.restart, schedule=sm)
                 e1.record()
                 torch.cuda.synchronize()
                 if i >= 3:
