@@ -691,9 +691,26 @@ def sweep(cfg, vol, rays, hits, stream, flush, args):
             t_ms = statistics.median(ms)
             o = hits[:n].cpu().numpy()
             nb, _ = compare(o[idx, :3], o[idx, 3].view(np.float32), ref)
+            t_sched = None
+            if not incoh:  # the same frames with VF_TRACE_SCHEDULE (order from the previous frame)
+                for _ in range(3):
+                    h.trace(rays, hits[:n], restart=restart, schedule=True)
+                ms = []
+                for i in range(7):
+                    flush.fill_(i)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    h.trace(rays, hits[:n], restart=restart, schedule=True)
+                    b.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(a.elapsed_time(b))
+                t_sched = statistics.median(ms)
+                o = hits[:n].cpu().numpy()
+                nb += compare(o[idx, :3], o[idx, 3].view(np.float32), ref)[0]
             out.append({"format": h.signature, "variant": "restart" if restart else "stack",
                         "kernel": "compiled-in" if st.get("compiled_in") else "generic",
                         "mrays_s": round(n / (t_ms / 1e3) / 1e6, 1),
+                        "mrays_s_scheduled": round(n / (t_sched / 1e3) / 1e6, 1) if t_sched else None,
                         "bytes_per_voxel": round(st["bytes_used"] / st["nonempty_voxels"], 4),
                         "paper_bytes_per_voxel": round(st["paper_layout_bytes"] / st["nonempty_voxels"], 4),
                         "mib": round(st["bytes_used"] / 2**20, 1), "alg_bytes_per_ray": round(alg / n, 1),

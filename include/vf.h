@@ -195,8 +195,9 @@ enum {
                                    keeps 8 B per block + 8 B per ray for up to 32 arrays (least recently used
                                    evicted; allocated through the build's vf_allocator); launches
                                    sharing an array are ordered by an event (inside stream capture
-                                   the graph orders them, and an array first seen during capture
-                                   runs unscheduled). Coherent-ray launches only (not with
+                                   the graph orders them, an array first seen during capture runs
+                                   unscheduled, and an array used in a capture keeps its schedule
+                                   memory until vf_destroy). Coherent-ray launches only (not with
                                    VF_TRACE_INCOHERENT, whose persistent warps balance by design). */
   VF_TRACE_REGROUP = 1u << 3,    /* with VF_TRACE_SCHEDULE: also regroup the rays into warps.
                                    Inside every group of 256 consecutive rays (a 16x16 screen tile

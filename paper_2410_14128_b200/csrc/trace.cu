@@ -1775,8 +1775,11 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
       return nullptr;
     }
     if ((uint64_t)nb <= 2ull * (uint64_t)per_sm * (uint64_t)sms) return nullptr;
-    for (auto& x : h->sched)  // an empty slot, else the least recently used one
+    for (auto& x : h->sched) {  // an empty slot, else the least recently used unpinned one
+      if (x.pinned) continue;
       if (!e || !x.mem || (e->mem && x.last_use < e->last_use)) e = &x;
+    }
+    if (!e) return nullptr;  // every entry belongs to a captured graph
     if (e->mem) {  // evict: no launch may still use its memory
       if (e->ev) cudaEventSynchronize(e->ev);
       h->alloc.put(e->mem, e->bytes, s);
@@ -1799,6 +1802,8 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
     cudaMemsetAsync(e->mem + 2 * (size_t)nb, 0, (2 * kSchedBuckets + 1) * sizeof(uint32_t), s);
   } else if (!capturing) {
     cudaStreamWaitEvent(s, e->ev, 0);  // after the launch that wrote cost (any stream)
+  } else {
+    e->pinned = true;  // the graph being captured reads and writes this entry on every replay
   }
   e->last_use = ++h->sched_clock;
   uint32_t* cost = e->mem;

@@ -129,6 +129,7 @@ struct SchedEntry {
   size_t bytes = 0;
   cudaEvent_t ev = nullptr;   // recorded after the last launch that wrote cost (cross-stream order)
   bool valid = false;         // cost holds a completed launch's durations
+  bool pinned = false;        // used inside a stream capture: a graph may replay it, never evicted
   uint64_t last_use = 0;
 };
 constexpr int kSchedEntries = 32;

@@ -108,6 +108,16 @@ def test_schedule_inside_cuda_graph():
         hits.zero_()
         g.replay()
         _check(torch, hits, ref, f"graph replay {it}")
+    # 34 more arrays push every other entry out (LRU over 32); the captured array's entry is pinned
+    others = [rt.clone() for _ in range(34)]
+    for o in others:
+        for _ in range(2):
+            h.trace(o, schedule=True)
+    torch.cuda.synchronize()
+    del others
+    hits.zero_()
+    g.replay()
+    _check(torch, hits, ref, "graph replay after LRU pressure")
     # an array first seen during capture runs unscheduled (nothing is allocated during capture)
     rt2 = rt.clone()
     hits2 = torch.empty_like(hits)

@@ -24,3 +24,11 @@ for r in sorted(stack.values(), key=lambda r: r["paper_bytes_per_voxel"]):
     gain = f"{rs['mrays_s'] / r['mrays_s']:.2f}x" if rs else "—"
     print(f"| {r['format']} | {r['paper_bytes_per_voxel']} | {r['mrays_s']} | {'**yes**' if r['format'] in front else ''} | {gain} |")
 print(f"\nfrontier: {', '.join(front)}")
+if any(r.get("mrays_s_scheduled") for r in stack.values()):  # the same with VF_TRACE_SCHEDULE
+    front_s, best = [], -1.0
+    for r in sorted(stack.values(), key=lambda r: (r["paper_bytes_per_voxel"], -(r.get("mrays_s_scheduled") or 0))):
+        if (r.get("mrays_s_scheduled") or 0) > best:
+            front_s.append(r["format"])
+            best = r["mrays_s_scheduled"]
+    print(f"\nwith VF_TRACE_SCHEDULE (Mrays/s scheduled): frontier: " + ", ".join(
+        f"{f} ({stack[f]['mrays_s_scheduled']})" for f in front_s))
