@@ -22,6 +22,7 @@ ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--counters", action="store_true")
 ap.add_argument("--align", action="store_true", help="build with VF_BUILD_ALIGN_NODES")
 ap.add_argument("--schedule", action="store_true", help="VF_TRACE_SCHEDULE launches (launch 2+ are ordered)")
+ap.add_argument("--regroup", action="store_true", help="+ VF_TRACE_REGROUP (rays regrouped into warps)")
 a = ap.parse_args()
 vname, _, deffmt, _ = bench.CONFIGS[a.config]
 vol = bench.make_volume(vname)
@@ -37,6 +38,6 @@ if a.counters:
     n = c["rays"]
     print({k: round(v / n, 4) for k, v in c.items()})
 for _ in range(a.reps):
-    h.trace(rays, hits, restart=a.restart, schedule=a.schedule)
+    h.trace(rays, hits, restart=a.restart, schedule="regroup" if a.regroup else a.schedule)
 torch.cuda.synchronize()
 print(h.signature, h.stats()["bytes_used"])
