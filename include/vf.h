@@ -199,15 +199,19 @@ enum {
                                    unscheduled, and an array used in a capture keeps its schedule
                                    memory until vf_destroy). Coherent-ray launches only (not with
                                    VF_TRACE_INCOHERENT, whose persistent warps balance by design). */
-  VF_TRACE_REGROUP = 1u << 3,    /* with VF_TRACE_SCHEDULE: also regroup the rays into warps.
+  VF_TRACE_REGROUP = 1u << 3,    /* with VF_TRACE_SCHEDULE: may also regroup the rays into warps.
                                    Inside every group of 256 consecutive rays (a 16x16 screen tile
                                    of a tile-ordered ray stream) the rays are ordered by their
                                    iteration counts in the previous launch over the array, longest
-                                   first, so the lanes of a warp end together. Pays when the rays
-                                   repeat (a static view: +5-8 % on top of the schedule), costs up
-                                   to 10 % when the camera moves between launches (the per-ray
-                                   counts no longer match and warps lose their 8x4-pixel shape).
-                                   Results are identical. */
+                                   first, so the lanes of a warp end together. This pays when the
+                                   rays repeat (a static view) and costs when the camera moves or
+                                   warps lose too much pixel coherence, so it is MEASURED: the
+                                   library times its own launches over the array (CUDA events,
+                                   queried without blocking), alternating schedule-only and
+                                   regrouped launches, keeps the faster mode, and re-measures every
+                                   256 launches; a launch captured into a graph keeps the faster
+                                   mode measured so far (schedule-only before any measurement).
+                                   Results are identical either way. */
   /* bit 30 is reserved (internal ablation: persistent warps with dynamic ray refill) */
 };
 

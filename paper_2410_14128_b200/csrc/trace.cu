@@ -1799,6 +1799,12 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
     e->n = n;
     e->nb = nb;
     e->valid = false;
+    for (int i = 0; i < 4; ++i) e->tmode[i] = -1;  // (a new array: its own measurements)
+    e->ms_sum[0] = e->ms_sum[1] = 0.0;
+    e->ms_n[0] = e->ms_n[1] = 0;
+    e->decided = -1;
+    e->since = 0;
+    e->last_mode = 0;
     cudaMemsetAsync(e->mem + 2 * (size_t)nb, 0, (2 * kSchedBuckets + 1) * sizeof(uint32_t), s);
   } else if (!capturing) {
     cudaStreamWaitEvent(s, e->ev, 0);  // after the launch that wrote cost (any stream)
@@ -1806,6 +1812,55 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
     e->pinned = true;  // the graph being captured reads and writes this entry on every replay
   }
   e->last_use = ++h->sched_clock;
+  e->pending = -1;
+  int mode = 0;  // 1: regroup the rays into warps this launch
+  if (regroup) {
+    constexpr uint32_t kReeval = 256;
+    if (!capturing) {
+      for (int i = 0; i < 4; ++i)  // harvest the timings of completed launches (never blocks)
+        if (e->tmode[i] >= 0) {
+          const cudaError_t q = cudaEventQuery(e->t1[i]);
+          if (q == cudaSuccess) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, e->t0[i], e->t1[i]) == cudaSuccess) {
+              e->ms_sum[e->tmode[i]] += ms;
+              e->ms_n[e->tmode[i]] += 1;
+            }
+            e->tmode[i] = -1;
+          }
+          cudaGetLastError();  // (cudaErrorNotReady is not an error here)
+        }
+    }
+    if (e->decided >= 0 && e->since >= kReeval) {  // re-measure now and then
+      e->decided = -1;
+      e->since = 0;
+      e->ms_sum[0] = e->ms_sum[1] = 0.0;
+      e->ms_n[0] = e->ms_n[1] = 0;
+    }
+    // regrouping must win by 2 % (it moves rays away from their 8x4-pixel warps: when in doubt, don't)
+    const bool rg_faster = e->ms_n[0] && e->ms_n[1] && e->ms_sum[1] / e->ms_n[1] < 0.98 * (e->ms_sum[0] / e->ms_n[0]);
+    if (e->decided < 0 && e->ms_n[0] >= 2 && e->ms_n[1] >= 2) e->decided = rg_faster ? 1 : 0;
+    if (e->decided >= 0) {
+      mode = e->decided;
+    } else if (capturing) {  // a graph keeps one mode: the faster so far, else the plain schedule
+      mode = rg_faster ? 1 : 0;
+    } else {
+      mode = (int)(e->since & 1u);  // measuring: alternate the two modes
+    }
+    ++e->since;
+    if (!capturing && e->valid) {  // time this launch (order kernels + trace)
+      const int i = e->tnext;
+      e->tnext = (i + 1) & 3;
+      bool ok = true;
+      if (!e->t0[i]) ok = cudaEventCreate(&e->t0[i]) == cudaSuccess && cudaEventCreate(&e->t1[i]) == cudaSuccess;
+      if (ok && e->tmode[i] < 0 && cudaEventRecord(e->t0[i], s) == cudaSuccess) {
+        e->tmode[i] = (int8_t)mode;
+        e->pending = i;
+      }
+      cudaGetLastError();
+    }
+  }
+  e->last_mode = mode;
   uint32_t* cost = e->mem;
   uint32_t* order = e->mem + nb;
   uint32_t* hist = e->mem + 2 * (size_t)nb;
@@ -1823,7 +1878,7 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
     sched_scatter_kernel<<<g, 256, 0, s>>>(cost, nb, hist, hist + kSchedBuckets, hist + 2 * kSchedBuckets, order,
                                            cfg);
     tp.order = order;
-    if (regroup) {
+    if (mode == 1) {
       sched_raysort_kernel<<<(unsigned)((n + kRayGroup - 1) / kRayGroup), kRayGroup, 0, s>>>(ray_cost, n, ray_perm);
       tp.ray_perm = ray_perm;
     }
@@ -1839,7 +1894,7 @@ uint32_t trace_launch_count(const Handle* h, const vf_ray* rays, uint64_t n, uin
     return 1;
   std::lock_guard<std::mutex> lk(h->sched_mu);
   for (const auto& x : h->sched)
-    if (x.mem && x.rays == rays && x.n == n && x.valid) return (flags & VF_TRACE_REGROUP) ? 4 : 3;
+    if (x.mem && x.rays == rays && x.n == n && x.valid) return (flags & VF_TRACE_REGROUP) && x.last_mode ? 4 : 3;
   return 1;
 }
 
@@ -1848,6 +1903,10 @@ void free_schedules(const Handle* h) {
   for (auto& x : h->sched) {
     if (x.mem) h->alloc.put(x.mem, x.bytes, h->build_stream);
     if (x.ev) cudaEventDestroy(x.ev);
+    for (int i = 0; i < 4; ++i) {
+      if (x.t0[i]) cudaEventDestroy(x.t0[i]);
+      if (x.t1[i]) cudaEventDestroy(x.t1[i]);
+    }
     x = SchedEntry{};
   }
 }
@@ -1951,6 +2010,10 @@ vf_status launch_trace(const Handle* h, const vf_ray* rays, uint64_t n, vf_hit* 
     fn<<<(unsigned)blocks, threads, 0, s>>>(tp, h->buf, reinterpret_cast<const float4*>(rays),
                                             reinterpret_cast<int4*>(hits), n, counters, nullptr);
     if (se && !capturing && cudaEventRecord(se->ev, s) == cudaSuccess) se->valid = true;
+    if (se && !capturing && se->pending >= 0 && cudaEventRecord(se->t1[se->pending], s) != cudaSuccess) {
+      cudaGetLastError();
+      se->tmode[se->pending] = -1;
+    }
 #ifdef VF_BLOCK_CLOCK
     if (const char* out = getenv("VF_BLOCK_CLOCK_OUT")) {
       std::vector<unsigned long long> hb(3 * blocks);

@@ -130,6 +130,18 @@ struct SchedEntry {
   cudaEvent_t ev = nullptr;   // recorded after the last launch that wrote cost (cross-stream order)
   bool valid = false;         // cost holds a completed launch's durations
   bool pinned = false;        // used inside a stream capture: a graph may replay it, never evicted
+  // VF_TRACE_REGROUP is measured, not assumed: the library times its own launches over this array
+  // (events around the order kernels + trace), alternating "block schedule only" (mode 0) and
+  // "+ ray regrouping" (mode 1), and then keeps the faster mode (re-measured every kReeval launches)
+  cudaEvent_t t0[4] = {}, t1[4] = {};
+  int8_t tmode[4] = {-1, -1, -1, -1};  // mode timed by event pair i (-1: none pending)
+  int tnext = 0;                       // next event pair
+  int pending = -1;                    // event pair of the launch being issued (t1 recorded after it)
+  double ms_sum[2] = {0.0, 0.0};
+  int ms_n[2] = {0, 0};
+  int decided = -1;      // faster mode, or -1 while measuring
+  uint32_t since = 0;    // launches since the decision / measuring launches
+  int last_mode = 0;     // mode of the last launch (vf_trace_launch_count)
   uint64_t last_use = 0;
 };
 constexpr int kSchedEntries = 32;

@@ -66,10 +66,11 @@ def test_scheduled_launches_equal_oracle(mode):
     torch, vf, h, rays, ref = _setup()
     rt = torch.from_numpy(rays).cuda()
     for restart in (False, True):
-        for it in range(4):  # launch 0: index order; 1..3: ordered by the previous launch
+        for it in range(8):  # launch 0: index order; then ordered (regroup: both modes measured)
             hits = h.trace(rt, restart=restart, schedule=mode)
             _check(torch, hits, ref, f"schedule={mode} launch {it} restart={restart}")
-            assert h.launch_count(rt, restart=restart, schedule=mode) == (4 if mode == "regroup" else 3)
+            # (regrouping is measured: a launch regroups or not, 4 or 3 kernels)
+            assert h.launch_count(rt, restart=restart, schedule=mode) in ((3, 4) if mode == "regroup" else (3,))
     h.close()
 
 

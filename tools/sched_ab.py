@@ -42,17 +42,21 @@ for cfg in a.configs:
     rays_np = bench.make_rays(cfg)[0]
     rays = torch.from_numpy(rays_np).cuda()
     prev = {f: torch.from_numpy(moved_rays(CAM[cfg], f)).cuda() for f in (0.005, 0.05)}
+    path = [torch.from_numpy(moved_rays(CAM[cfg], 0.001 * j)).cuda() for j in range(a.reps + 3)]
     n = rays.shape[0]
     buf = torch.empty_like(rays)
     hits = torch.empty((n, 4), dtype=torch.int32, device="cuda")
     ref = h.trace(rays).clone()
     res = {}
     for rep in range(2):
-        for mode in ("natural", "sched", "regroup", "moved-0.005", "moved-0.005-regroup"):
+        for mode in ("natural", "sched", "regroup", "moved-0.005", "moved-0.005-regroup", "path-sched",
+                     "path-regroup"):
             ms = []
             for i in range(a.reps + 3):
                 sm = "regroup" if mode.endswith("regroup") else mode != "natural"
-                if mode.startswith("moved"):
+                if mode.startswith("path"):  # a moving camera: frame i of a path of 0.1 % steps
+                    buf.copy_(path[i % len(path)])
+                elif mode.startswith("moved"):
                     buf.copy_(prev[float(mode.split("-")[1])])
                     h.trace(buf, hits, restart=a.restart, schedule=sm)
                     buf.copy_(rays)
@@ -66,7 +70,8 @@ for cfg in a.configs:
                 torch.cuda.synchronize()
                 if i >= 3:
                     ms.append(e0.elapsed_time(e1))
-                assert torch.equal(hits, ref), f"{cfg} {mode}: hits differ"
+                if not mode.startswith("path"):
+                    assert torch.equal(hits, ref), f"{cfg} {mode}: hits differ"
             res.setdefault(mode, []).append(statistics.median(ms))
     base = min(res["natural"])
     print(f"{cfg} {h.signature} {'restart' if a.restart else 'stack'} ({n} rays): " + ", ".join(
