@@ -1415,9 +1415,24 @@ __global__ void __launch_bounds__(256) sched_scatter_kernel(const uint32_t* __re
   __syncthreads();
   for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) atomicAdd(&loc[sched_class(cost, nb, i, g)], 1u);
   __syncthreads();
-  if (threadIdx.x < kSchedBuckets) {  // class start (exclusive scan of hist) + this CTA's range in it
-    uint32_t start = 0;
-    for (uint32_t k = 0; k < threadIdx.x; ++k) start += hist[k];
+  // class start (exclusive scan of hist: one class per thread of the first kSchedBuckets, warp
+  // shuffles + the warp totals) + this CTA's range in it
+  __shared__ uint32_t wtot[kSchedBuckets / 32];
+  uint32_t hv = 0, incl = 0;
+  if (threadIdx.x < kSchedBuckets) {
+    hv = hist[threadIdx.x];
+    incl = hv;
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if ((threadIdx.x & 31u) >= d) incl += y;
+    }
+    if ((threadIdx.x & 31u) == 31u) wtot[threadIdx.x >> 5] = incl;
+  }
+  __syncthreads();
+  if (threadIdx.x < kSchedBuckets) {
+    uint32_t start = incl - hv;
+    for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) start += wtot[w];
     const uint32_t cnt = loc[threadIdx.x];
     base[threadIdx.x] = start + (cnt ? atomicAdd(&cursor[threadIdx.x], cnt) : 0u);
     loc[threadIdx.x] = 0;
