@@ -24,6 +24,7 @@ per-format sweep (--sweep) goes to a file under profiles/, never into that line.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import socket
@@ -591,6 +592,7 @@ def run_ours(args):
                        "variant": ("restart" if args.restart else "stack") + ("+incoherent" if incoh else ""),
                        "kernel": "compiled-in" if stats.get("compiled_in") else "generic",
                        "volume": list(dims), "rays_per_frame": n_total, "nonempty_voxels": nonempty,
+                       "rays_sha256": hashlib.sha256(np.ascontiguousarray(rays_all).tobytes()).hexdigest()[:16],
                        "bytes_used": stats["bytes_used"], "bytes_per_voxel": round(stats["bytes_used"] / nonempty, 4),
                        "bytes_per_voxel_paper": round(stats["paper_layout_bytes"] / nonempty, 4),
                        "hit_rate": round(float((gxyz[:, 0] >= 0).mean()), 4), "build_s": round(build_s, 3),
@@ -635,7 +637,9 @@ def run_ours(args):
             hb = step.hits if step.hits is not None else torch.empty((rays.shape[0], 4), dtype=torch.int32, device=dev)
             rows = sweep(cfg, vol, rays, hb, stream, flush, args)
             with open(out, "w") as f:
-                json.dump({"config": cfg, "rows": rows, "clocks": clk}, f, indent=1)
+                json.dump({"config": cfg, "rows": rows, "clocks": clk,
+                           "rays_sha256": hashlib.sha256(np.ascontiguousarray(rays_all).tobytes()).hexdigest()}, f,
+                          indent=1)
             result["sweep_file"] = os.path.relpath(out, ROOT)
     if dist_on:
         dist.barrier()

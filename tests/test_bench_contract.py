@@ -68,6 +68,7 @@ def test_driver_command_prints_one_compact_json_line():
         assert d.get(k), k
     assert d["cpu_baseline"]["parity_mismatches"] == 0 and d["cpu_baseline"]["parity_checked"] > 0
     assert 0 < d["roofline"]["frac"] < 1 and d["e2e"]["h2d_bytes_per_step"] == 32 * d["config"]["rays_per_frame"]
+    assert len(d["config"]["rays_sha256"]) == 16  # every ray buffer recorded by its SHA-256
 
 
 def test_gpus_mismatch_exits_nonzero():
