@@ -50,9 +50,13 @@ def _check(cfg, fmts, incoherent=False):
     hits = torch.empty((len(rays), 4), dtype=torch.int32, device="cuda")
     for fmt, h in _handles(vol, fmts):
         for restart in (False, True):
-            h.trace(rt, hits, restart=restart, incoherent=incoherent)  # as bench.py launches it
-            out = hits.cpu().numpy()
-            assert_parity(out[:, :3], out[:, 3].view(np.float32), ref, f"{cfg} {fmt} restart={restart} (full frame)")
+            # as bench.py launches it: VF_TRACE_SCHEDULE for coherent rays — the first launch over the
+            # array runs in index order and records block durations, the second runs reordered
+            for launch in range(1 if incoherent else 2):
+                h.trace(rt, hits, restart=restart, incoherent=incoherent, schedule=not incoherent)
+                out = hits.cpu().numpy()
+                assert_parity(out[:, :3], out[:, 3].view(np.float32), ref,
+                              f"{cfg} {fmt} restart={restart} launch {launch} (full frame)")
 
 
 def test_cfg1_full_frame():
@@ -103,11 +107,12 @@ def test_cfg4s_secondary_full_frame():
     hits = torch.empty((len(rays), 4), dtype=torch.int32, device="cuda")
     for fmt, h in _handles(vol, bench.SWEEP["cfg4s"]):
         for restart in (False, True):
-            for incoh in (False, True):  # bench.py's launch (plain) and the VF_TRACE_INCOHERENT kernel
-                h.trace(rt, hits, restart=restart, incoherent=incoh)
-                out = hits.cpu().numpy()
-                assert_parity(out[:, :3], out[:, 3].view(np.float32), ref,
-                              f"cfg4s {fmt} restart={restart} incoherent={incoh} (full frame)")
+            for incoh in (False, True):  # bench.py's launch (plain, scheduled) and the VF_TRACE_INCOHERENT kernel
+                for launch in range(1 if incoh else 2):
+                    h.trace(rt, hits, restart=restart, incoherent=incoh, schedule=not incoh)
+                    out = hits.cpu().numpy()
+                    assert_parity(out[:, :3], out[:, 3].view(np.float32), ref,
+                                  f"cfg4s {fmt} restart={restart} incoherent={incoh} launch {launch} (full frame)")
 
 
 def test_cfg5_full_frame_every_sweep_format():
@@ -133,3 +138,25 @@ def test_cfg5_tile_sharded_frame_assembled(tmp_path):
                        capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "FRAME OK" in r.stdout
+
+
+def test_cfg4_street_view_full_frame():
+    """SURVEY §8(d) cfg4 "plus a street-level view": eye 40 voxels above the street, looking along
+    it (long grazing rays between the buildings), 960x540, every ray vs the oracle."""
+    import torch
+    import bench
+    from inputs import rays as R
+    vol = bench.make_volume("city")
+    rays, _ = R.camera("city_street", scale=2)
+    g = oracle.Grid.from_generator(vol)
+    ref = g.trace(rays)
+    g.close()
+    rt = torch.from_numpy(rays).cuda()
+    hits = torch.empty((len(rays), 4), dtype=torch.int32, device="cuda")
+    for fmt, h in _handles(vol, ["R(4, 4, 4) G(7)", "G(11)", "S(11)", "T(2, 4) R(3, 3, 3)", "D(4, 4, 4, 6) G(7)"]):
+        for restart in (False, True):
+            for launch in range(2):
+                h.trace(rt, hits, restart=restart, schedule=True)
+                out = hits.cpu().numpy()
+                assert_parity(out[:, :3], out[:, 3].view(np.float32), ref,
+                              f"street {fmt} restart={restart} launch {launch}")
