@@ -53,6 +53,8 @@ CONFIGS = {
     # shadow + AO rays spawned from the cfg4 primary hits (SURVEY §8(f) NEXT 3 as specified)
     "cfg4s": ("city", "secondary", "R(4, 4, 4) G(7)",
               "2048^3 city, shadow + AO rays spawned from the 1920x1080 aerial primary hits"),
+    # SURVEY §8(d) cfg4 "plus a street-level view": grazing rays along the street (not a BASELINE config)
+    "cfg4st": ("city", "city_street", "R(4, 4, 4) G(7)", "2048^3 city, 1920x1080 street-level view"),
     # the paper's 512^3 Table 2 rows (21-40) on a 512^3 city (not a BASELINE config)
     "t512": ("city512", "city512", "R(4, 4, 4) G(5)", "512^3 synthetic city blocks, 1024x1024 rays (Table 2 rows 21-40)"),
 }

@@ -4,7 +4,8 @@ import numpy as np
 
 from inputs import rays as R
 
-CAM = {"cfg2": "menger", "cfg3": "terrain", "cfg4": "city", "cfg5": "sparse", "t512": "city512"}
+CAM = {"cfg2": "menger", "cfg3": "terrain", "cfg4": "city", "cfg5": "sparse", "t512": "city512",
+       "cfg4st": "city_street"}
 
 
 def moved_rays(cam, frac):
