@@ -192,7 +192,7 @@ enum {
                                    The first launch over an array runs in index order, and so does
                                    every launch of at most two waves of resident blocks (nothing to
                                    reorder). The handle
-                                   keeps 8 B per block + 8 B per ray for up to 32 arrays (least recently used
+                                   keeps 9 B per block + 8 B per ray for up to 32 arrays (least recently used
                                    evicted; allocated through the build's vf_allocator); launches
                                    sharing an array are ordered by an event (inside stream capture
                                    the graph orders them, an array first seen during capture runs

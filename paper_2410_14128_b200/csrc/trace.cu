@@ -1392,28 +1392,33 @@ __device__ __forceinline__ uint32_t sched_class(const uint32_t* __restrict__ cos
 }
 
 __global__ void __launch_bounds__(256) sched_hist_kernel(const uint32_t* __restrict__ cost, uint32_t nb,
-                                                         uint32_t* __restrict__ hist, SchedCfg g) {
+                                                         uint32_t* __restrict__ hist, uint8_t* __restrict__ cls,
+                                                         SchedCfg g) {
   __shared__ uint32_t sh[kSchedBuckets];
   for (uint32_t i = threadIdx.x; i < kSchedBuckets; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x)
-    atomicAdd(&sh[sched_class(cost, nb, i, g)], 1u);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const uint32_t k = sched_class(cost, nb, i, g);  // (kept for the scatter: one byte per block)
+    cls[i] = (uint8_t)k;
+    atomicAdd(&sh[k], 1u);
+  }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < kSchedBuckets; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
-__global__ void __launch_bounds__(256) sched_scatter_kernel(const uint32_t* __restrict__ cost, uint32_t nb,
+__global__ void __launch_bounds__(256) sched_scatter_kernel(const uint8_t* __restrict__ cls, uint32_t nb,
                                                             uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor,
                                                             uint32_t* __restrict__ done, uint32_t* __restrict__ order,
                                                             SchedCfg g) {
+  (void)g;  // (the classes were computed with it by sched_hist_kernel)
   __shared__ uint32_t base[kSchedBuckets], loc[kSchedBuckets];
   __shared__ bool last;
   const uint32_t per = (nb + gridDim.x - 1) / gridDim.x;
   const uint32_t b0 = blockIdx.x * per, b1 = min(nb, b0 + per);
   if (threadIdx.x < kSchedBuckets) loc[threadIdx.x] = 0;
   __syncthreads();
-  for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) atomicAdd(&loc[sched_class(cost, nb, i, g)], 1u);
+  for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) atomicAdd(&loc[__ldg(cls + i)], 1u);
   __syncthreads();
   // class start (exclusive scan of hist: one class per thread of the first kSchedBuckets, warp
   // shuffles + the warp totals) + this CTA's range in it
@@ -1439,7 +1444,7 @@ __global__ void __launch_bounds__(256) sched_scatter_kernel(const uint32_t* __re
   }
   __syncthreads();
   for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-    const uint32_t k = sched_class(cost, nb, i, g);
+    const uint32_t k = __ldg(cls + i);
     order[base[k] + atomicAdd(&loc[k], 1u)] = i;
   }
   // the last CTA to finish resets hist / cursor / done for the next launch (every CTA has read hist)
@@ -1800,7 +1805,7 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
       h->alloc.put(e->mem, e->bytes, s);
       e->mem = nullptr;
     }
-    const size_t words = 2 * (size_t)nb + 2 * kSchedBuckets + 1 + 2 * (size_t)n;
+    const size_t words = 2 * (size_t)nb + 2 * kSchedBuckets + 1 + 2 * (size_t)n + ((size_t)nb + 3) / 4;
     e->mem = static_cast<uint32_t*>(h->alloc.get(words * sizeof(uint32_t), s));
     if (!e->mem) return nullptr;
     if (!e->ev && cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming) != cudaSuccess) {
@@ -1881,6 +1886,7 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
   uint32_t* hist = e->mem + 2 * (size_t)nb;
   uint32_t* ray_cost = hist + 2 * kSchedBuckets + 1;
   uint32_t* ray_perm = ray_cost + n;
+  uint8_t* cls = reinterpret_cast<uint8_t*>(ray_perm + n);  // per-block duration class
   if (e->valid) {
     const unsigned g = (unsigned)std::min<uint32_t>(148u, (nb + 255u) / 256u);
     static const SchedCfg cfg = [] {  // A/B knobs (tools/sched_ab.py): VF_SCHED_SUB, VF_SCHED_DIL
@@ -1889,8 +1895,8 @@ SchedEntry* prepare_schedule(const Handle* h, const vf_ray* rays, uint64_t n, ui
       if (const char* e = getenv("VF_SCHED_DIL")) c.dil = (uint32_t)std::min(16, std::max(0, atoi(e)));
       return c;
     }();
-    sched_hist_kernel<<<g, 256, 0, s>>>(cost, nb, hist, cfg);
-    sched_scatter_kernel<<<g, 256, 0, s>>>(cost, nb, hist, hist + kSchedBuckets, hist + 2 * kSchedBuckets, order,
+    sched_hist_kernel<<<g, 256, 0, s>>>(cost, nb, hist, cls, cfg);
+    sched_scatter_kernel<<<g, 256, 0, s>>>(cls, nb, hist, hist + kSchedBuckets, hist + 2 * kSchedBuckets, order,
                                            cfg);
     tp.order = order;
     if (mode == 1) {
