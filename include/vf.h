@@ -114,7 +114,7 @@ typedef struct {
 } vf_volume;
 
 /* ---------------------------------------------------------------- build */
-typedef struct vf_handle vf_handle; /* opaque; owns the format buffer; immutable after build */
+typedef struct vf_handle vf_handle; /* opaque; owns the format buffer (immutable after build) and the trace-schedule cache */
 
 /* Device memory provider ("PyTorch only for device memory and streams"; the
  * Python binding passes torch's caching allocator). Every device allocation of vf_build (the
@@ -191,9 +191,9 @@ enum {
                                    blocks run changes: every ray is traced, results are identical.
                                    The first launch over an array runs in index order, and so does
                                    every launch of at most two waves of resident blocks (nothing to
-                                   reorder). The handle
-                                   keeps 9 B per block + 8 B per ray for up to 32 arrays (least recently used
-                                   evicted; allocated through the build's vf_allocator); launches
+                                   reorder). The handle keeps 9 B per block + 8 B per ray for up
+                                   to 32 arrays (least recently used evicted; allocated through
+                                   the build's vf_allocator); launches
                                    sharing an array are ordered by an event (inside stream capture
                                    the graph orders them, an array first seen during capture runs
                                    unscheduled, and an array used in a capture keeps its schedule
@@ -217,7 +217,8 @@ enum {
 
 /* Trace n rays (device array) into hits (device array), one thread per ray, asynchronously
  * on cuda_stream; hits are valid after the stream synchronises. Concurrent traces on one
- * handle are allowed (read-only). n = 0 is a no-op. Formats of the library's compiled-in list
+ * handle are allowed (the format buffer is read-only; VF_TRACE_SCHEDULE's per-array state is
+ * guarded by a lock and ordered across streams by events). n = 0 is a no-op. Formats of the library's compiled-in list
  * (the paper's per-format generated code: R(A^3) G(M), G(L), S(L), T(n,d),
  * S(a) G(b), D(A^3,M) over S/G, the cfg2/cfg3 headline formats, single Raw grids) run a kernel
  * with the format's tier geometry compiled in; all others the generic tier-table kernel.
@@ -227,7 +228,8 @@ VF_API vf_status vf_trace(const vf_handle* h, const vf_ray* rays, uint64_t n, vf
 
 /* Kernel launches one vf_trace / vf_trace_ex / vf_trace_scatter call with these arguments makes
  * now (host-side query, no GPU work): 3 when VF_TRACE_SCHEDULE will reorder it (the two order
- * kernels + the trace; 4 with VF_TRACE_REGROUP), else 1. For launch accounting (bench.py). */
+ * kernels + the trace; 4 when VF_TRACE_REGROUP currently regroups), else 1. For launch
+ * accounting (bench.py). */
 VF_API vf_status vf_trace_launch_count(const vf_handle* h, const vf_ray* rays, uint64_t n, uint32_t trace_flags,
                                        uint32_t* count);
 
